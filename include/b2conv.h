@@ -1,0 +1,188 @@
+/*
+ * b2conv — B200-native fp32 forward convolution (cuConv, arXiv 2103.16234),
+ * C ABI.  Everything crossing this boundary is POD: int32/int64 scalars,
+ * plain structs, raw float pointers and an opaque stream handle.  No C++ or
+ * torch types appear here.
+ *
+ * The reference (convkit 0.1.0, /root/reference/pkg/src/convkit) has no FFI of
+ * its own; it is pure Python.  Each entry point below names the reference
+ * interface it replaces (file:line), and INTEGRATION.md shows the ctypes
+ * binding a reference maintainer would add.
+ *
+ * Conventions
+ *  - Tensors are NCHW fp32, C-contiguous: input [n][c][h][w], filters
+ *    [m][c][hf][wf], output [n][m][ho][wo] with ho = (h+2ph-hf)/stride+1
+ *    (configs.py:60-64).  Cross-correlation, no dilation/groups/bias.
+ *  - `y` is always fully overwritten, never accumulated into.
+ *  - Device entry points are asynchronous on `stream` (a cudaStream_t; NULL =
+ *    legacy default stream) and never allocate.  *_host entry points take host
+ *    buffers and are synchronous.
+ *  - Errors: a b2c_status is returned and a thread-local message is available
+ *    from b2c_last_error().  The Python layer maps statuses onto the
+ *    reference's exception classes (errors.py:9-61) in the reference's
+ *    precedence: Unsupported(stride) -> ShapeMismatch -> InvalidPlan ->
+ *    WorkspaceExceeded (twostage.py:73-79, 214-224).
+ *  - Results are bitwise independent of the tile plan and of how a batch is
+ *    sharded across GPUs (each output's summation order depends only on
+ *    c, hf, wf), mirroring SPEC.md:315,326.
+ */
+#ifndef B2CONV_H
+#define B2CONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2C_ABI_VERSION 1
+
+/* == ConvConfig without its name (configs.py:17-40). */
+typedef struct {
+  int32_t n, c, h, w, m, hf, wf, stride, pad_h, pad_w;
+} b2c_conv_desc;
+
+typedef enum {
+  B2C_OK = 0,
+  B2C_UNSUPPORTED = 1,         /* errors.Unsupported (errors.py:41-42)          */
+  B2C_SHAPE_MISMATCH = 2,      /* errors.ShapeMismatch (errors.py:45-46)        */
+  B2C_INVALID_PLAN = 3,        /* errors.InvalidPlan (errors.py:49-50)          */
+  B2C_WORKSPACE_EXCEEDED = 4,  /* errors.WorkspaceExceeded (errors.py:53-61)    */
+  B2C_INVALID_CONFIG = 5,      /* errors.InvalidConfig (errors.py:29-34)        */
+  B2C_CUDA_ERROR = 6,          /* a CUDA runtime failure (no reference analogue) */
+  B2C_INVALID_ARGUMENT = 7     /* null pointer / bad enum (no reference analogue) */
+} b2c_status;
+
+/* == execmodel.DeviceModel (execmodel.py:36-56). */
+typedef struct {
+  int32_t warp_width, line_bytes, max_threads_per_block, element_bytes;
+} b2c_device_model;
+
+/* == execmodel.LaunchPlan (execmodel.py:59-66). */
+typedef struct {
+  int64_t blocks;
+  int32_t threads_per_block, split_per_filter_row, dot_products_per_thread;
+} b2c_launch_plan;
+
+/* == twostage.RunStats (twostage.py:48-55); counts follow the reference's
+ * launch-plan arithmetic so the reference's stat tests hold. */
+typedef struct {
+  int64_t stage1_tasks_run;
+  int32_t stage2_invoked;
+  int64_t filter_row_global_loads;
+  int64_t workspace_bytes;
+} b2c_run_stats;
+
+/* The B200 tile plan chosen by the planner (no reference analogue: the
+ * reference's model has one filter row per block; this is the real grid). */
+typedef struct {
+  int32_t family;       /* kernel family id, see b2c_family_name()          */
+  int32_t bm;           /* output channels per CTA                          */
+  int32_t bp;           /* output pixels per CTA (flattened n,y,x)          */
+  int32_t bc;           /* input channels per pipeline stage                */
+  int32_t threads;      /* threads per CTA                                  */
+  int32_t stages;       /* cp.async pipeline depth                          */
+  int32_t smem_rows;    /* halo rows staged per channel                     */
+  int32_t smem_row_stride;
+  int32_t smem_bytes;   /* dynamic shared memory per CTA                    */
+  int64_t grid;         /* CTAs per launch                                  */
+} b2c_tile_plan;
+
+typedef enum {
+  B2C_ENGINE_FUSED = 0,    /* single-pass FFMA2 direct convolution, no workspace,
+                              within tol(K) = 1e-5*max(1,K/4096) of conv_naive_f64 */
+  B2C_ENGINE_TWOSTAGE = 1  /* paper-faithful stage 1 + stage 2 with the
+                              reference's separate-rounding order: bitwise equal
+                              to conv_naive / conv_twostage                      */
+} b2c_engine;
+
+/* ---------------------------------------------------------------- metadata */
+int32_t b2c_abi_version(void);
+const char *b2c_last_error(void);
+const char *b2c_family_name(int32_t family);
+int32_t b2c_num_families(void);
+/* 1 if kernel family `family` can run `d` under `engine` (used to enumerate
+ * tile plans in plan-independence tests). */
+int32_t b2c_family_matches(const b2c_conv_desc *d, int32_t engine, int32_t family);
+/* Number of CUDA kernel launches issued by this thread since the last reset
+ * (instrumentation used by bench.py's gpu_launches). */
+int64_t b2c_launch_count(void);
+void b2c_reset_launch_count(void);
+
+/* ------------------------------------------------------ shape / plan logic */
+/* ConvConfig.__post_init__ (configs.py:42-54); on failure *bad_field receives
+ * the index of the offending field in b2c_conv_desc order (n=0 .. pad_w=9). */
+b2c_status b2c_validate_config(const b2c_conv_desc *d, int32_t *bad_field);
+/* configs.output_dims (configs.py:60-64). */
+b2c_status b2c_output_dims(const b2c_conv_desc *d, int32_t *ho, int32_t *wo);
+/* twostage.workspace_bytes (twostage.py:36-45): 4*hf*wf*n*m*ho*wo, 0 for 1x1. */
+int64_t b2c_workspace_bytes(const b2c_conv_desc *d);
+/* execmodel.plan_launch (execmodel.py:73-98).  dev may be NULL (defaults). */
+b2c_status b2c_plan_launch(const b2c_conv_desc *d, const b2c_device_model *dev, b2c_launch_plan *out);
+/* execmodel.validate_plan (execmodel.py:101-123). */
+b2c_status b2c_validate_plan(const b2c_conv_desc *d, const b2c_device_model *dev, const b2c_launch_plan *p);
+/* execmodel.block_position_ranges (execmodel.py:126-128): writes 2*split
+ * int64 values lo0,hi0,lo1,hi1,... */
+b2c_status b2c_block_position_ranges(int64_t work, int64_t split, int64_t *lo_hi);
+/* B200 tile planner for the given engine ("launch planner picks the tile shape
+ * per (filter size, channels, spatial size, batch)").  If out->family >= 0 on
+ * entry that family is forced (B2C_INVALID_PLAN if it cannot run d). */
+b2c_status b2c_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tile_plan *out);
+
+/* ------------------------------------------------- device-pointer compute */
+/* Fused direct convolution (any stride >= 1, any padding).  Replaces the
+ * compute of twostage.conv_twostage (twostage.py:208-239) and
+ * reference.conv_naive (reference.py:58-83) for device-resident tensors.
+ * `tiles` may be NULL (planner's choice). */
+b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const float *w, float *y,
+                              const b2c_tile_plan *tiles, void *stream);
+
+/* twostage.conv_twostage (twostage.py:208-239): preconditions in the
+ * reference's order, then stage 1 (+ stage 2 unless 1x1) with the reference's
+ * rounding order.  `plan` may be NULL (plan_launch default).  `workspace`
+ * must hold b2c_workspace_bytes(d) bytes (may be NULL for 1x1). */
+b2c_status b2c_conv_twostage(const b2c_conv_desc *d, const float *x, const float *w, float *y,
+                             float *workspace, int64_t workspace_size, const b2c_launch_plan *plan,
+                             const b2c_device_model *dev, int64_t workspace_limit, void *stream,
+                             b2c_run_stats *stats);
+
+/* twostage.stage1_scalar_prods (twostage.py:148-172): partials laid out
+ * (k, n, m, ho, wo), k = yf*wf+xf; partials must hold 4*hf*wf*n*m*ho*wo bytes. */
+b2c_status b2c_stage1_scalar_prods(const b2c_conv_desc *d, const float *x, const float *w, float *partials,
+                                   const b2c_launch_plan *plan, const b2c_device_model *dev,
+                                   int64_t workspace_limit, void *stream, b2c_run_stats *stats);
+
+/* twostage.stage2_sum (twostage.py:175-205): y = +0 + sum_k partials[k]. */
+b2c_status b2c_stage2_sum(const b2c_conv_desc *d, const float *partials, float *y, void *stream,
+                          b2c_run_stats *stats);
+
+/* --------------------------------------------------- host-buffer compute */
+/* The drop-in for callers holding host (numpy) buffers: copies x and w to the
+ * device, runs `engine`, copies y back, synchronises.  Device buffers are
+ * cached per thread and grown on demand.  For B2C_ENGINE_TWOSTAGE the
+ * reference preconditions, plan and workspace limit apply exactly as in
+ * b2c_conv_twostage; for B2C_ENGINE_FUSED stride >= 1 is accepted and no
+ * workspace is used.  device < 0 means the current device. */
+b2c_status b2c_conv_host(const b2c_conv_desc *d, const float *x_host, const float *w_host, float *y_host,
+                         int32_t engine, const b2c_launch_plan *plan, const b2c_device_model *dev,
+                         int64_t workspace_limit, int32_t device, b2c_run_stats *stats);
+
+/* Host-buffer stage 1 / stage 2 (used by the drop-in stage1_scalar_prods /
+ * stage2_sum). */
+b2c_status b2c_stage1_host(const b2c_conv_desc *d, const float *x_host, const float *w_host,
+                           float *partials_host, const b2c_launch_plan *plan, const b2c_device_model *dev,
+                           int64_t workspace_limit, int32_t device, b2c_run_stats *stats);
+b2c_status b2c_stage2_host(const b2c_conv_desc *d, const float *partials_host, float *y_host,
+                           int32_t device, b2c_run_stats *stats);
+
+/* Pinned host memory helpers (so e2e callers can stage through page-locked
+ * buffers without linking CUDA themselves). */
+void *b2c_host_alloc(size_t bytes);
+void b2c_host_free(void *p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* B2CONV_H */

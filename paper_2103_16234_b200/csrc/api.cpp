@@ -1,0 +1,563 @@
+// C ABI of the B200 forward-convolution engine (include/b2conv.h).
+//
+// Host-side responsibilities: the reference's preconditions and their order
+// (twostage.py:73-79, 214-224), the reference planner's arithmetic for the
+// drop-in RunStats / InvalidPlan contract (execmodel.py:73-128), the B200 tile
+// plan cache, and host<->device staging for callers that hold host buffers.
+#include "../../include/b2conv.h"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "internal.h"
+
+namespace {
+
+thread_local std::string t_last_error;
+std::atomic<long long> g_launches{0};
+
+b2c_status fail(b2c_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_last_error = buf;
+  return st;
+}
+
+b2c_status cuda_fail(cudaError_t e, const char *what) {
+  return fail(B2C_CUDA_ERROR, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+const char *kFieldNames[] = {"n", "c", "h", "w", "m", "hf", "wf", "stride", "pad_h", "pad_w"};
+
+const int32_t *fields_of(const b2c_conv_desc *d) { return &d->n; }
+
+b2c_status check_config(const b2c_conv_desc *d, int32_t *bad_field) {
+  if (!d) return fail(B2C_INVALID_ARGUMENT, "null descriptor");
+  const int32_t *f = fields_of(d);
+  for (int i = 0; i < 8; i++) {
+    if (f[i] < 1) {
+      if (bad_field) *bad_field = i;
+      return fail(B2C_INVALID_CONFIG, "%s: must be >= 1, got %d", kFieldNames[i], f[i]);
+    }
+  }
+  for (int i = 8; i < 10; i++) {
+    if (f[i] < 0) {
+      if (bad_field) *bad_field = i;
+      return fail(B2C_INVALID_CONFIG, "%s: must be >= 0, got %d", kFieldNames[i], f[i]);
+    }
+  }
+  if ((long long)d->hf > (long long)d->h + 2LL * d->pad_h) {
+    if (bad_field) *bad_field = 5;
+    return fail(B2C_INVALID_CONFIG, "hf: filter height %d exceeds padded input height %lld", d->hf,
+                (long long)d->h + 2LL * d->pad_h);
+  }
+  if ((long long)d->wf > (long long)d->w + 2LL * d->pad_w) {
+    if (bad_field) *bad_field = 6;
+    return fail(B2C_INVALID_CONFIG, "wf: filter width %d exceeds padded input width %lld", d->wf,
+                (long long)d->w + 2LL * d->pad_w);
+  }
+  return B2C_OK;
+}
+
+b2c::Geom geom_of(const b2c_conv_desc *d) {
+  b2c::Geom g;
+  g.N = d->n; g.C = d->c; g.H = d->h; g.W = d->w; g.M = d->m;
+  g.HF = d->hf; g.WF = d->wf; g.S = d->stride; g.PH = d->pad_h; g.PW = d->pad_w;
+  g.Ho = (d->h + 2 * d->pad_h - d->hf) / d->stride + 1;
+  g.Wo = (d->w + 2 * d->pad_w - d->wf) / d->stride + 1;
+  g.HoWo = g.Ho * g.Wo;
+  g.Hp = d->h + 2 * d->pad_h;
+  g.Wp = d->w + 2 * d->pad_w;
+  g.Q = (long long)g.N * g.HoWo;
+  return g;
+}
+
+b2c_status check_sizes(const b2c::Geom &g) {
+  const long long in = (long long)g.N * g.C * g.H * g.W;
+  const long long out = (long long)g.N * g.M * g.HoWo;
+  if (g.Q >= (1LL << 31) || (long long)g.N * g.Hp + g.Hp >= (1LL << 31) || in >= (1LL << 40) || out >= (1LL << 40))
+    return fail(B2C_UNSUPPORTED, "problem too large for the engine's index arithmetic");
+  return B2C_OK;
+}
+
+b2c_device_model default_device() { return b2c_device_model{32, 128, 1024, 4}; }
+
+b2c_status check_device(const b2c_device_model *dev) {
+  const int32_t *f = &dev->warp_width;
+  const char *names[] = {"warp_width", "line_bytes", "max_threads_per_block", "element_bytes"};
+  for (int i = 0; i < 4; i++)
+    if (f[i] < 1) return fail(B2C_INVALID_CONFIG, "%s: must be >= 1, got %d", names[i], f[i]);
+  if (dev->line_bytes % dev->element_bytes != 0)
+    return fail(B2C_INVALID_CONFIG, "line_bytes: %d not a multiple of element size %d", dev->line_bytes,
+                dev->element_bytes);
+  return B2C_OK;
+}
+
+// --------------------------------------------------------------- plan cache
+struct PlanKey {
+  b2c_conv_desc d;
+  int stage1;
+  int device;
+  int forced;
+  bool operator==(const PlanKey &o) const {
+    return std::memcmp(&d, &o.d, sizeof(d)) == 0 && stage1 == o.stage1 && device == o.device && forced == o.forced;
+  }
+};
+struct PlanKeyHash {
+  size_t operator()(const PlanKey &k) const {
+    size_t h = 1469598103934665603ULL;
+    const unsigned char *p = reinterpret_cast<const unsigned char *>(&k);
+    for (size_t i = 0; i < sizeof(PlanKey); i++) h = (h ^ p[i]) * 1099511628211ULL;
+    return h;
+  }
+};
+std::mutex g_plan_mu;
+std::unordered_map<PlanKey, b2c::TileChoice, PlanKeyHash> g_plans;
+
+b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, int forced, b2c::TileChoice *tc) {
+  int device = 0;
+  cudaGetDevice(&device);
+  PlanKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.d = *d;
+  key.stage1 = stage1;
+  key.device = device;
+  key.forced = forced;
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) {
+      *tc = it->second;
+      return B2C_OK;
+    }
+  }
+  if (!b2c::plan_tiles(g, stage1, device, forced, tc)) {
+    if (forced >= 0)
+      return fail(B2C_INVALID_PLAN, "tile family %d (%s) cannot run this configuration", forced,
+                  b2c::family_name(forced));
+    return fail(B2C_UNSUPPORTED, "no kernel family fits this configuration (shared-memory halo too large)");
+  }
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  g_plans[key] = *tc;
+  return B2C_OK;
+}
+
+void export_tiles(const b2c::TileChoice &tc, b2c_tile_plan *out) {
+  out->family = tc.family;
+  out->bm = tc.bm;
+  out->bp = tc.bp;
+  out->bc = tc.bc;
+  out->threads = tc.threads;
+  out->stages = tc.stages;
+  out->smem_rows = tc.rows;
+  out->smem_row_stride = tc.rs;
+  out->smem_bytes = tc.smem_bytes;
+  out->grid = tc.grid * tc.grid_z;
+}
+
+b2c_status resolve_plan(const b2c_conv_desc *d, const b2c_launch_plan *plan, const b2c_device_model *dev,
+                        b2c_launch_plan *resolved) {
+  if (plan) {
+    b2c_status st = b2c_validate_plan(d, dev, plan);
+    if (st != B2C_OK) return st;
+    *resolved = *plan;
+    return B2C_OK;
+  }
+  b2c_status st = b2c_plan_launch(d, dev, resolved);
+  if (st != B2C_OK) return st;
+  return b2c_validate_plan(d, dev, resolved);
+}
+
+// The reference's precondition order for conv_twostage / stage1_scalar_prods:
+// stride (Unsupported) -> [shape checks done by the caller] -> plan -> workspace.
+b2c_status twostage_preconditions(const b2c_conv_desc *d, const b2c_launch_plan *plan, const b2c_device_model *dev,
+                                  int64_t workspace_limit, b2c_launch_plan *resolved) {
+  b2c_status st = check_config(d, nullptr);
+  if (st != B2C_OK) return st;
+  if (d->stride != 1)
+    return fail(B2C_UNSUPPORTED, "two-stage convolution requires stride 1, got %d", d->stride);
+  st = resolve_plan(d, plan, dev, resolved);
+  if (st != B2C_OK) return st;
+  const int64_t need = b2c_workspace_bytes(d);
+  if (need > workspace_limit)
+    return fail(B2C_WORKSPACE_EXCEEDED, "workspace of %lld bytes exceeds limit of %lld bytes", (long long)need,
+                (long long)workspace_limit);
+  return B2C_OK;
+}
+
+void fill_stats(const b2c_conv_desc *d, const b2c_launch_plan &p, bool stage2, b2c_run_stats *s) {
+  if (!s) return;
+  s->stage1_tasks_run = p.blocks;
+  s->filter_row_global_loads = p.blocks;
+  s->stage2_invoked = stage2 ? 1 : 0;
+  s->workspace_bytes = stage2 ? b2c_workspace_bytes(d) : 0;
+}
+
+b2c_status run_stage1(const b2c_conv_desc *d, const b2c::Geom &g, const float *x, const float *w, float *out,
+                      cudaStream_t stream) {
+  b2c::TileChoice tc;
+  b2c_status st = get_tiles(d, g, true, -1, &tc);
+  if (st != B2C_OK) return st;
+  cudaError_t e = b2c::launch_direct(g, tc, x, w, out, true, (long long)g.N * g.M * g.HoWo, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "stage-1 launch");
+  return B2C_OK;
+}
+
+// ------------------------------------------------------ host staging cache
+struct DeviceBuffers {
+  void *ptr[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t cap[4] = {0, 0, 0, 0};
+  cudaStream_t stream = nullptr;
+};
+thread_local std::unordered_map<int, DeviceBuffers> t_bufs;
+
+b2c_status ensure(DeviceBuffers &b, int slot, size_t bytes) {
+  if (bytes == 0) bytes = 4;
+  if (b.cap[slot] >= bytes) return B2C_OK;
+  if (b.ptr[slot]) cudaFree(b.ptr[slot]);
+  b.ptr[slot] = nullptr;
+  b.cap[slot] = 0;
+  cudaError_t e = cudaMalloc(&b.ptr[slot], bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  b.cap[slot] = bytes;
+  return B2C_OK;
+}
+
+b2c_status select_device(int32_t device, DeviceBuffers **out) {
+  if (device >= 0) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  }
+  int cur = 0;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  DeviceBuffers &b = t_bufs[cur];
+  if (!b.stream) {
+    e = cudaStreamCreateWithFlags(&b.stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+  }
+  *out = &b;
+  return B2C_OK;
+}
+
+b2c_status sync_and_check(cudaStream_t s, const char *what) {
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  return B2C_OK;
+}
+
+}  // namespace
+
+namespace b2c {
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace b2c
+
+extern "C" {
+
+int32_t b2c_abi_version(void) { return B2C_ABI_VERSION; }
+const char *b2c_last_error(void) { return t_last_error.c_str(); }
+const char *b2c_family_name(int32_t family) { return b2c::family_name(family); }
+int32_t b2c_num_families(void) { return b2c::num_families(); }
+int64_t b2c_launch_count(void) { return g_launches.load(); }
+void b2c_reset_launch_count(void) { g_launches.store(0); }
+
+b2c_status b2c_validate_config(const b2c_conv_desc *d, int32_t *bad_field) { return check_config(d, bad_field); }
+
+b2c_status b2c_output_dims(const b2c_conv_desc *d, int32_t *ho, int32_t *wo) {
+  b2c_status st = check_config(d, nullptr);
+  if (st != B2C_OK) return st;
+  if (ho) *ho = (d->h + 2 * d->pad_h - d->hf) / d->stride + 1;
+  if (wo) *wo = (d->w + 2 * d->pad_w - d->wf) / d->stride + 1;
+  return B2C_OK;
+}
+
+int64_t b2c_workspace_bytes(const b2c_conv_desc *d) {
+  if (!d) return -1;
+  if (d->hf == 1 && d->wf == 1) return 0;
+  const int64_t ho = (d->h + 2 * d->pad_h - d->hf) / d->stride + 1;
+  const int64_t wo = (d->w + 2 * d->pad_w - d->wf) / d->stride + 1;
+  return 4LL * d->hf * d->wf * d->n * d->m * ho * wo;
+}
+
+b2c_status b2c_plan_launch(const b2c_conv_desc *d, const b2c_device_model *dev, b2c_launch_plan *out) {
+  if (!d || !out) return fail(B2C_INVALID_ARGUMENT, "null argument");
+  if (d->stride != 1) return fail(B2C_UNSUPPORTED, "launch planning covers stride 1, got %d", d->stride);
+  const b2c_device_model dm = dev ? *dev : default_device();
+  b2c_status st = check_device(&dm);
+  if (st != B2C_OK) return st;
+  const int64_t ho = (d->h + 2 * d->pad_h - d->hf) / d->stride + 1;
+  const int64_t wo = (d->w + 2 * d->pad_w - d->wf) / d->stride + 1;
+  const int64_t work = (int64_t)d->n * ho * wo;
+  const int64_t maxt = dm.max_threads_per_block, warp = dm.warp_width;
+  const int64_t split = (work + maxt - 1) / maxt;
+  int64_t threads = work < maxt ? work : maxt;
+  threads = (threads + warp - 1) / warp * warp;
+  if (threads > maxt) {
+    // device limit not a warp multiple: largest warp multiple under it
+    threads = maxt / warp * warp;
+    if (threads < warp) threads = warp;
+    if (threads > maxt) threads = maxt;
+  }
+  out->blocks = (int64_t)d->m * d->hf * d->wf * split;
+  out->threads_per_block = (int32_t)threads;
+  out->split_per_filter_row = (int32_t)split;
+  out->dot_products_per_thread = (int32_t)((work + split * threads - 1) / (split * threads));
+  return B2C_OK;
+}
+
+b2c_status b2c_validate_plan(const b2c_conv_desc *d, const b2c_device_model *dev, const b2c_launch_plan *p) {
+  if (!d || !p) return fail(B2C_INVALID_ARGUMENT, "null argument");
+  const b2c_device_model dm = dev ? *dev : default_device();
+  const int64_t ho = (d->h + 2 * d->pad_h - d->hf) / d->stride + 1;
+  const int64_t wo = (d->w + 2 * d->pad_w - d->wf) / d->stride + 1;
+  const int64_t work = (int64_t)d->n * ho * wo;
+  if (p->split_per_filter_row < 1)
+    return fail(B2C_INVALID_PLAN, "split_per_filter_row must be >= 1, got %d", p->split_per_filter_row);
+  const int64_t want_blocks = (int64_t)d->m * d->hf * d->wf * p->split_per_filter_row;
+  if (p->blocks != want_blocks)
+    return fail(B2C_INVALID_PLAN, "blocks %lld != m*hf*wf*split = %lld", (long long)p->blocks,
+                (long long)want_blocks);
+  if (p->threads_per_block < 1 || p->threads_per_block > dm.max_threads_per_block)
+    return fail(B2C_INVALID_PLAN, "threads_per_block %d outside [1, %d]", p->threads_per_block,
+                dm.max_threads_per_block);
+  if (p->threads_per_block % dm.warp_width != 0)
+    return fail(B2C_INVALID_PLAN, "threads_per_block %d not a multiple of warp width %d", p->threads_per_block,
+                dm.warp_width);
+  if (p->dot_products_per_thread < 1) return fail(B2C_INVALID_PLAN, "dot_products_per_thread must be >= 1");
+  const long double covered = (long double)p->blocks * p->threads_per_block * p->dot_products_per_thread;
+  const long double total = (long double)d->m * d->hf * d->wf * work;
+  if (covered < total)
+    return fail(B2C_INVALID_PLAN, "plan covers %.0Lf dot products, workload needs %.0Lf", covered, total);
+  return B2C_OK;
+}
+
+b2c_status b2c_block_position_ranges(int64_t work, int64_t split, int64_t *lo_hi) {
+  if (!lo_hi || split < 1) return fail(B2C_INVALID_ARGUMENT, "bad arguments");
+  for (int64_t i = 0; i < split; i++) {
+    lo_hi[2 * i] = i * work / split;
+    lo_hi[2 * i + 1] = (i + 1) * work / split;
+  }
+  return B2C_OK;
+}
+
+b2c_status b2c_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tile_plan *out) {
+  if (!out) return fail(B2C_INVALID_ARGUMENT, "null argument");
+  b2c_status st = check_config(d, nullptr);
+  if (st != B2C_OK) return st;
+  b2c::Geom g = geom_of(d);
+  if ((st = check_sizes(g)) != B2C_OK) return st;
+  if (engine == B2C_ENGINE_TWOSTAGE && d->stride != 1)
+    return fail(B2C_UNSUPPORTED, "two-stage convolution requires stride 1, got %d", d->stride);
+  b2c::TileChoice tc;
+  st = get_tiles(d, g, engine == B2C_ENGINE_TWOSTAGE, out->family >= 0 ? out->family : -1, &tc);
+  if (st != B2C_OK) return st;
+  export_tiles(tc, out);
+  return B2C_OK;
+}
+
+int32_t b2c_family_matches(const b2c_conv_desc *d, int32_t engine, int32_t family) {
+  if (check_config(d, nullptr) != B2C_OK) return 0;
+  return b2c::family_matches(family, geom_of(d), engine == B2C_ENGINE_TWOSTAGE) ? 1 : 0;
+}
+
+b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const float *w, float *y,
+                              const b2c_tile_plan *tiles, void *stream) {
+  b2c_status st = check_config(d, nullptr);
+  if (st != B2C_OK) return st;
+  if (!x || !w || !y) return fail(B2C_INVALID_ARGUMENT, "null tensor pointer");
+  b2c::Geom g = geom_of(d);
+  if ((st = check_sizes(g)) != B2C_OK) return st;
+  b2c::TileChoice tc;
+  st = get_tiles(d, g, false, (tiles && tiles->family >= 0) ? tiles->family : -1, &tc);
+  if (st != B2C_OK) return st;
+  cudaError_t e = b2c::launch_direct(g, tc, x, w, y, false, 0, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fused conv launch");
+  return B2C_OK;
+}
+
+b2c_status b2c_stage1_scalar_prods(const b2c_conv_desc *d, const float *x, const float *w, float *partials,
+                                   const b2c_launch_plan *plan, const b2c_device_model *dev,
+                                   int64_t workspace_limit, void *stream, b2c_run_stats *stats) {
+  b2c_launch_plan rp;
+  b2c_status st = twostage_preconditions(d, plan, dev, workspace_limit, &rp);
+  if (st != B2C_OK) return st;
+  if (!x || !w || !partials) return fail(B2C_INVALID_ARGUMENT, "null tensor pointer");
+  b2c::Geom g = geom_of(d);
+  if ((st = check_sizes(g)) != B2C_OK) return st;
+  st = run_stage1(d, g, x, w, partials, (cudaStream_t)stream);
+  if (st != B2C_OK) return st;
+  if (stats) {
+    fill_stats(d, rp, false, stats);
+    stats->workspace_bytes = b2c_workspace_bytes(d);
+  }
+  return B2C_OK;
+}
+
+b2c_status b2c_stage2_sum(const b2c_conv_desc *d, const float *partials, float *y, void *stream,
+                          b2c_run_stats *stats) {
+  b2c_status st = check_config(d, nullptr);
+  if (st != B2C_OK) return st;
+  if (!partials || !y) return fail(B2C_INVALID_ARGUMENT, "null tensor pointer");
+  b2c::Geom g = geom_of(d);
+  int device = 0;
+  cudaGetDevice(&device);
+  cudaError_t e = b2c::launch_stage2(partials, y, (long long)g.N * g.M * g.HoWo, g.HF * g.WF, device,
+                                     (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "stage-2 launch");
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->stage2_invoked = 1;
+  }
+  return B2C_OK;
+}
+
+b2c_status b2c_conv_twostage(const b2c_conv_desc *d, const float *x, const float *w, float *y, float *workspace,
+                             int64_t workspace_size, const b2c_launch_plan *plan, const b2c_device_model *dev,
+                             int64_t workspace_limit, void *stream, b2c_run_stats *stats) {
+  b2c_launch_plan rp;
+  b2c_status st = twostage_preconditions(d, plan, dev, workspace_limit, &rp);
+  if (st != B2C_OK) return st;
+  if (!x || !w || !y) return fail(B2C_INVALID_ARGUMENT, "null tensor pointer");
+  b2c::Geom g = geom_of(d);
+  if ((st = check_sizes(g)) != B2C_OK) return st;
+  const bool one_by_one = d->hf == 1 && d->wf == 1;
+  if (one_by_one) {
+    // fused 1x1: stage 1 writes the output directly, no workspace (twostage.py:228-231)
+    st = run_stage1(d, g, x, w, y, (cudaStream_t)stream);
+    if (st != B2C_OK) return st;
+  } else {
+    const int64_t need = b2c_workspace_bytes(d);
+    if (!workspace || workspace_size < need)
+      return fail(B2C_INVALID_ARGUMENT, "workspace of %lld bytes required, %lld provided", (long long)need,
+                  (long long)workspace_size);
+    st = run_stage1(d, g, x, w, workspace, (cudaStream_t)stream);
+    if (st != B2C_OK) return st;
+    int device = 0;
+    cudaGetDevice(&device);
+    cudaError_t e = b2c::launch_stage2(workspace, y, (long long)g.N * g.M * g.HoWo, g.HF * g.WF, device,
+                                       (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "stage-2 launch");
+  }
+  fill_stats(d, rp, !one_by_one, stats);
+  return B2C_OK;
+}
+
+b2c_status b2c_conv_host(const b2c_conv_desc *d, const float *x_host, const float *w_host, float *y_host,
+                         int32_t engine, const b2c_launch_plan *plan, const b2c_device_model *dev,
+                         int64_t workspace_limit, int32_t device, b2c_run_stats *stats) {
+  b2c_status st = check_config(d, nullptr);
+  if (st != B2C_OK) return st;
+  if (engine != B2C_ENGINE_FUSED && engine != B2C_ENGINE_TWOSTAGE)
+    return fail(B2C_INVALID_ARGUMENT, "unknown engine %d", engine);
+  if (!x_host || !w_host || !y_host) return fail(B2C_INVALID_ARGUMENT, "null tensor pointer");
+  b2c_launch_plan rp;
+  if (engine == B2C_ENGINE_TWOSTAGE) {
+    st = twostage_preconditions(d, plan, dev, workspace_limit, &rp);
+    if (st != B2C_OK) return st;
+  }
+  b2c::Geom g = geom_of(d);
+  if ((st = check_sizes(g)) != B2C_OK) return st;
+  DeviceBuffers *b = nullptr;
+  if ((st = select_device(device, &b)) != B2C_OK) return st;
+  const size_t xb = sizeof(float) * (size_t)g.N * g.C * g.H * g.W;
+  const size_t wb = sizeof(float) * (size_t)g.M * g.C * g.HF * g.WF;
+  const size_t yb = sizeof(float) * (size_t)g.N * g.M * g.HoWo;
+  const size_t wsb = engine == B2C_ENGINE_TWOSTAGE ? (size_t)b2c_workspace_bytes(d) : 0;
+  if ((st = ensure(*b, 0, xb)) || (st = ensure(*b, 1, wb)) || (st = ensure(*b, 2, yb)) ||
+      (wsb && (st = ensure(*b, 3, wsb))))
+    return st;
+  cudaError_t e = cudaMemcpyAsync(b->ptr[0], x_host, xb, cudaMemcpyHostToDevice, b->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(b->ptr[1], w_host, wb, cudaMemcpyHostToDevice, b->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "host-to-device copy");
+  const float *dx = static_cast<const float *>(b->ptr[0]);
+  const float *dw = static_cast<const float *>(b->ptr[1]);
+  float *dy = static_cast<float *>(b->ptr[2]);
+  if (engine == B2C_ENGINE_FUSED) {
+    st = b2c_conv2d_forward(d, dx, dw, dy, nullptr, b->stream);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+  } else {
+    st = b2c_conv_twostage(d, dx, dw, dy, static_cast<float *>(b->ptr[3]), (int64_t)wsb, &rp, dev,
+                           workspace_limit, b->stream, stats);
+  }
+  if (st != B2C_OK) return st;
+  e = cudaMemcpyAsync(y_host, dy, yb, cudaMemcpyDeviceToHost, b->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "device-to-host copy");
+  return sync_and_check(b->stream, "convolution");
+}
+
+b2c_status b2c_stage1_host(const b2c_conv_desc *d, const float *x_host, const float *w_host, float *partials_host,
+                           const b2c_launch_plan *plan, const b2c_device_model *dev, int64_t workspace_limit,
+                           int32_t device, b2c_run_stats *stats) {
+  b2c_launch_plan rp;
+  b2c_status st = twostage_preconditions(d, plan, dev, workspace_limit, &rp);
+  if (st != B2C_OK) return st;
+  if (!x_host || !w_host || !partials_host) return fail(B2C_INVALID_ARGUMENT, "null tensor pointer");
+  b2c::Geom g = geom_of(d);
+  if ((st = check_sizes(g)) != B2C_OK) return st;
+  DeviceBuffers *b = nullptr;
+  if ((st = select_device(device, &b)) != B2C_OK) return st;
+  const size_t xb = sizeof(float) * (size_t)g.N * g.C * g.H * g.W;
+  const size_t wb = sizeof(float) * (size_t)g.M * g.C * g.HF * g.WF;
+  const size_t pb = sizeof(float) * (size_t)g.HF * g.WF * g.N * g.M * g.HoWo;
+  if ((st = ensure(*b, 0, xb)) || (st = ensure(*b, 1, wb)) || (st = ensure(*b, 3, pb))) return st;
+  cudaError_t e = cudaMemcpyAsync(b->ptr[0], x_host, xb, cudaMemcpyHostToDevice, b->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(b->ptr[1], w_host, wb, cudaMemcpyHostToDevice, b->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "host-to-device copy");
+  st = run_stage1(d, g, static_cast<const float *>(b->ptr[0]), static_cast<const float *>(b->ptr[1]),
+                  static_cast<float *>(b->ptr[3]), b->stream);
+  if (st != B2C_OK) return st;
+  e = cudaMemcpyAsync(partials_host, b->ptr[3], pb, cudaMemcpyDeviceToHost, b->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "device-to-host copy");
+  if (stats) {
+    fill_stats(d, rp, false, stats);
+    stats->workspace_bytes = b2c_workspace_bytes(d);
+  }
+  return sync_and_check(b->stream, "stage 1");
+}
+
+b2c_status b2c_stage2_host(const b2c_conv_desc *d, const float *partials_host, float *y_host, int32_t device,
+                           b2c_run_stats *stats) {
+  b2c_status st = check_config(d, nullptr);
+  if (st != B2C_OK) return st;
+  if (!partials_host || !y_host) return fail(B2C_INVALID_ARGUMENT, "null tensor pointer");
+  b2c::Geom g = geom_of(d);
+  DeviceBuffers *b = nullptr;
+  if ((st = select_device(device, &b)) != B2C_OK) return st;
+  const size_t yb = sizeof(float) * (size_t)g.N * g.M * g.HoWo;
+  const size_t pb = yb * (size_t)g.HF * g.WF;
+  if ((st = ensure(*b, 2, yb)) || (st = ensure(*b, 3, pb))) return st;
+  cudaError_t e = cudaMemcpyAsync(b->ptr[3], partials_host, pb, cudaMemcpyHostToDevice, b->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "host-to-device copy");
+  st = b2c_stage2_sum(d, static_cast<const float *>(b->ptr[3]), static_cast<float *>(b->ptr[2]), b->stream, stats);
+  if (st != B2C_OK) return st;
+  e = cudaMemcpyAsync(y_host, b->ptr[2], yb, cudaMemcpyDeviceToHost, b->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "device-to-host copy");
+  return sync_and_check(b->stream, "stage 2");
+}
+
+void *b2c_host_alloc(size_t bytes) {
+  void *p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 4, cudaHostAllocPortable) != cudaSuccess) {
+    fail(B2C_CUDA_ERROR, "cudaHostAlloc of %zu bytes failed", bytes);
+    return nullptr;
+  }
+  return p;
+}
+
+void b2c_host_free(void *p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,254 @@
+// Kernel instantiations, the B200 tile planner and launch helpers.
+//
+// The reference plans one filter row per block with <=1024 threads
+// (execmodel.plan_launch, execmodel.py:73-98).  On B200 the planner instead
+// picks, per (filter size, stride, channels, spatial size, batch), a kernel
+// family (BM output channels x BP output pixels per CTA, BC channels per
+// pipeline stage) by minimising an occupancy- and wave-quantisation-aware cost
+// over the 148 SMs.  The reference plan is still computed and validated by the
+// C ABI for the drop-in's RunStats / InvalidPlan contract (api.cpp).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "conv_kernel.cuh"
+#include "internal.h"
+
+namespace b2c {
+
+namespace {
+
+struct Family {
+  const char *name;
+  int hf, wf, s;  // 0 = generic (runtime)
+  int bm, bp, bc;
+  bool strict;
+  int threads;
+  const void *kernel;
+  int max_ctas_per_sm;  // from __launch_bounds__
+};
+
+#define B2C_FAMILY(NAME, HF, WF, S, BM, BP, BC, STRICT)                                                    \
+  Family {                                                                                                 \
+    NAME, HF, WF, S, BM, BP, BC, STRICT, ConvTile<HF, WF, S, BM, BP, BC, STRICT>::NT,                     \
+        reinterpret_cast<const void *>(&conv_direct_kernel<HF, WF, S, BM, BP, BC, STRICT>),                \
+        (ConvTile<HF, WF, S, BM, BP, BC, STRICT>::NT >= 512 ? 1 : 2)                                       \
+  }
+
+const Family kFamilies[] = {
+    // fused FFMA2 families
+    B2C_FAMILY("fused_1x1s1_m32", 1, 1, 1, 32, 256, 16, false),
+    B2C_FAMILY("fused_1x1s1_m64", 1, 1, 1, 64, 256, 16, false),
+    B2C_FAMILY("fused_1x1s1_m128", 1, 1, 1, 128, 256, 16, false),
+    B2C_FAMILY("fused_1x1s2_m64", 1, 1, 2, 64, 256, 16, false),
+    B2C_FAMILY("fused_1x1s2_m128", 1, 1, 2, 128, 256, 16, false),
+    B2C_FAMILY("fused_3x3s1_m32", 3, 3, 1, 32, 256, 8, false),
+    B2C_FAMILY("fused_3x3s1_m64", 3, 3, 1, 64, 256, 8, false),
+    B2C_FAMILY("fused_3x3s1_m128", 3, 3, 1, 128, 256, 8, false),
+    B2C_FAMILY("fused_3x3s2_m64", 3, 3, 2, 64, 256, 8, false),
+    B2C_FAMILY("fused_3x3s2_m128", 3, 3, 2, 128, 256, 8, false),
+    B2C_FAMILY("fused_5x5s1_m32", 5, 5, 1, 32, 256, 4, false),
+    B2C_FAMILY("fused_5x5s1_m64", 5, 5, 1, 64, 256, 4, false),
+    B2C_FAMILY("fused_5x5s1_m128", 5, 5, 1, 128, 256, 4, false),
+    B2C_FAMILY("fused_7x7s2_m64", 7, 7, 2, 64, 256, 4, false),
+    B2C_FAMILY("fused_generic_m64", 0, 0, 0, 64, 256, 4, false),
+    B2C_FAMILY("fused_generic_m32", 0, 0, 0, 32, 256, 4, false),
+    // paper-faithful stage 1 (strict FMUL+FADD, one filter row per blockIdx.z)
+    B2C_FAMILY("stage1_strict_m32", 1, 1, 1, 32, 256, 16, true),
+    B2C_FAMILY("stage1_strict_m64", 1, 1, 1, 64, 256, 16, true),
+};
+constexpr int kNumFamilies = sizeof(kFamilies) / sizeof(kFamilies[0]);
+
+int g_sm_count = -1;
+std::mutex g_mu;
+bool g_attr_done[kNumFamilies][64] = {};
+
+int sm_count_of(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_sm_count > 0) return g_sm_count;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0) n = 148;
+  g_sm_count = n;
+  return n;
+}
+
+inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+
+// Rows of the virtual padded image stack needed by the worst tile.
+int max_tile_rows(const Geom &g, int hf_eff, int bp) {
+  const long long tiles = cdiv(g.Q, bp);
+  int worst = 0;
+  for (long long t = 0; t < tiles; t++) {
+    const long long qa = t * bp;
+    const long long qb = std::min<long long>(qa + bp, g.Q) - 1;
+    const long long na = qa / g.HoWo, nb = qb / g.HoWo;
+    const long long ya = (qa - na * g.HoWo) / g.Wo, yb = (qb - nb * g.HoWo) / g.Wo;
+    const long long rows = (nb * g.Hp + yb * g.S) - (na * g.Hp + ya * g.S) + hf_eff;
+    worst = (int)std::max<long long>(worst, rows);
+  }
+  return worst;
+}
+
+struct Candidate {
+  int family = -1;
+  TileChoice tc;
+  double cost = 1e300;
+};
+
+bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, Candidate *out) {
+  const Family &f = kFamilies[fam_id];
+  const int hf_eff = stage1 ? 1 : g.HF;
+  const int wf_eff = stage1 ? 1 : g.WF;
+  const int taps = hf_eff * wf_eff;
+  TileChoice tc;
+  tc.family = fam_id;
+  tc.bm = f.bm;
+  tc.bp = f.bp;
+  tc.bc = f.bc;
+  tc.threads = f.threads;
+  tc.rs = (g.Wo - 1) * g.S + wf_eff;
+  tc.rows = max_tile_rows(g, hf_eff, f.bp);
+  const long long tile_elems = (long long)tc.rs * tc.rows;
+  if (tile_elems > (1 << 20)) return false;
+  tc.tile_elems = (int)tile_elems;
+  tc.xcs = (int)((tile_elems + 3) & ~3LL);
+  const int nchunks = (int)cdiv(g.C, f.bc);
+  tc.stages = nchunks > 1 ? 2 : 1;
+  const long long stage_floats = (long long)f.bc * tc.xcs + (long long)f.bc * taps * (f.bm + 4);
+  const long long smem = 4LL * (tc.xcs + tc.stages * stage_floats);
+  if (smem > 227 * 1024) return false;
+  tc.smem_bytes = (int)smem;
+  // relative offsets inside a tile must fit int32 (goff table)
+  const long long imgs = cdiv(f.bp, g.HoWo) + 2;
+  if (imgs * (long long)g.C * g.H * g.W >= INT_MAX) return false;
+  const long long mtiles = cdiv(g.M, f.bm);
+  const long long ptiles = cdiv(g.Q, f.bp);
+  tc.grid = mtiles * ptiles;
+  tc.grid_z = stage1 ? g.HF * g.WF : 1;
+  const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
+  const int by_threads = 2048 / f.threads;
+  const int occ = std::max(1, std::min({f.max_ctas_per_sm, by_smem, by_threads}));
+  tc.occupancy = occ;
+  const long long total_ctas = tc.grid * tc.grid_z;
+  const double waves = (double)cdiv(total_ctas, (long long)sms * occ);
+  // per-CTA work: FMA lanes plus staging traffic (element loads ~ 8 FMA-lane equivalents)
+  const double fma = (double)f.bm * f.bp * taps * g.C;
+  const double loads = 8.0 * ((double)tile_elems + (double)f.bm * taps) * g.C;
+  const double per_cta = fma * (stage1 ? 2.0 : 1.0) + loads;
+  out->family = fam_id;
+  out->tc = tc;
+  out->cost = waves * occ * per_cta;
+  return true;
+}
+
+}  // namespace
+
+const char *family_name(int id) {
+  if (id < 0 || id >= kNumFamilies) return "invalid";
+  return kFamilies[id].name;
+}
+
+int num_families() { return kNumFamilies; }
+
+bool family_matches(int fam_id, const Geom &g, bool stage1) {
+  if (fam_id < 0 || fam_id >= kNumFamilies) return false;
+  const Family &f = kFamilies[fam_id];
+  if (f.strict != stage1) return false;
+  if (stage1) return g.S == 1;
+  if (f.hf == 0) return true;  // generic
+  return f.hf == g.HF && f.wf == g.WF && f.s == g.S;
+}
+
+int device_sm_count(int device) { return sm_count_of(device); }
+
+// Planner: returns false if no family can run the geometry.
+bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, TileChoice *out) {
+  const int sms = sm_count_of(device);
+  Candidate best;
+  bool exact_found = false;
+  if (forced_family >= 0) {
+    if (!family_matches(forced_family, g, stage1)) return false;
+    if (!evaluate(g, forced_family, stage1, sms, &best)) return false;
+    *out = best.tc;
+    return true;
+  }
+  for (int pass = 0; pass < 2; pass++) {
+    for (int i = 0; i < kNumFamilies; i++) {
+      const Family &f = kFamilies[i];
+      if (!family_matches(i, g, stage1)) continue;
+      const bool generic = (f.hf == 0) && !stage1;
+      if (pass == 0 && generic) continue;  // prefer specialised families
+      if (pass == 1 && !generic) continue;
+      Candidate c;
+      if (!evaluate(g, i, stage1, sms, &c)) continue;
+      if (c.cost < best.cost * 0.999 || (c.cost <= best.cost * 1.001 && best.family >= 0 &&
+                                         kFamilies[i].bm > kFamilies[best.family].bm))
+        best = c;
+      exact_found = true;
+    }
+    if (exact_found) break;
+  }
+  if (best.family < 0) return false;
+  *out = best.tc;
+  return true;
+}
+
+cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, const float *w, float *y,
+                          bool stage1, long long y_tap_stride, cudaStream_t stream) {
+  const Family &f = kFamilies[tc.family];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (dev < 64 && !g_attr_done[tc.family][dev]) {
+      cudaError_t e = cudaFuncSetAttribute(f.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      g_attr_done[tc.family][dev] = true;
+    }
+  }
+  KParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.x = x;
+  p.w = w;
+  p.y = y;
+  p.N = g.N; p.C = g.C; p.H = g.H; p.W = g.W; p.M = g.M;
+  p.S = g.S;
+  p.HF = stage1 ? 1 : g.HF;
+  p.WF = stage1 ? 1 : g.WF;
+  p.PH = g.PH; p.PW = g.PW;
+  p.Ho = g.Ho; p.Wo = g.Wo; p.HoWo = g.HoWo;
+  p.Hp = g.Hp;
+  p.Q = (int)g.Q;
+  p.RS = tc.rs;
+  p.ROWS = tc.rows;
+  p.XCS = tc.xcs;
+  p.tile_elems = tc.tile_elems;
+  p.mtiles = (int)cdiv(g.M, tc.bm);
+  p.nchunks = (int)cdiv(g.C, tc.bc);
+  p.w_ctaps = g.HF * g.WF;
+  p.wf_full = g.WF;
+  p.y_tap_stride = y_tap_stride;
+  p.strict_tap_major = stage1 ? 1 : 0;
+  void *args[] = {&p};
+  dim3 grid((unsigned)tc.grid, 1, (unsigned)tc.grid_z);
+  note_launch();
+  return cudaLaunchKernel(f.kernel, grid, dim3(tc.threads), args, (size_t)tc.smem_bytes, stream);
+}
+
+cudaError_t launch_stage2(const float *partials, float *y, long long total, int taps, int device,
+                          cudaStream_t stream) {
+  const int sms = sm_count_of(device);
+  const long long work = (total % 4 == 0) ? total / 4 : total;
+  long long blocks = std::min<long long>(cdiv(work, 256), (long long)sms * 8);
+  if (blocks < 1) blocks = 1;
+  note_launch();
+  stage2_sum_kernel<<<(unsigned)blocks, 256, 0, stream>>>(partials, y, total, taps);
+  return cudaGetLastError();
+}
+
+}  // namespace b2c
