@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 forward-convolution engine (the driver's contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2] [--batch B] [--engine fused|twostage]
+                    [--report PATH]        # per-layer sweep of all BASELINE configs
+
+A *step* is one pass of the hot path over one batch of synthetic input: every
+layer of the workload (default C2 = the 36 GoogLeNet inception 1x1 layers,
+BASELINE.json configs[1], at N=32 images per GPU) convolved once with its
+filter bank.  ``value`` is whole-job GFLOP/s (algorithmic flops
+2*N*M*Ho*Wo*C*hf*wf of all ranks / max-over-ranks device time of K steps, the
+K steps replayed as one CUDA graph per step with inputs resident in HBM).
+
+Also reported: ``e2e`` (same metric through the host-buffer C-ABI drop-in,
+H2D of inputs+filters and D2H of outputs inside the timed region),
+``roofline`` (FP32 FFMA-bound: algorithmic TFLOP/s of the conv kernels, from
+per-layer CUDA-event timings, over the FFMA2 peak measured live by
+``b2c_probe_fp32_peak``), ``cpu_baseline`` (the oracle's C port of the
+reference's conv_twostage on the host's cores), ``clocks`` (NVML during the
+timed region) and ``gpu_launches``.
+
+``--impl reference`` times the reference algorithm on the CPU (the oracle
+port of convkit.conv_twostage, all host threads) for the same metric/config;
+under torchrun only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.45: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz
+DEFAULT_BATCH = {"c1": 1, "c2": 32, "c3": 128, "c4": 8, "c5": 256}
+STRONG = {"c5"}  # ResNet-50 N=256 is split across GPUs (strong scaling)
+
+
+def parse():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5"), default="c2")
+    ap.add_argument("--batch", type=int, default=0, help="images per layer (per GPU, or global for c5)")
+    ap.add_argument("--engine", choices=("fused", "twostage"), default="fused")
+    ap.add_argument("--report", default="", help="write a per-layer sweep of every BASELINE config to PATH")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are best-effort metadata
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nv:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": sorted(self.reasons)}
+
+
+# --------------------------------------------------------------------------- CPU legs
+def cpu_run(cfgs, sample_batch, min_seconds, rng_seed=0):
+    """Time the oracle's C port of convkit.conv_twostage (stage 1 + stage 2,
+    the reference's algorithm and rounding) with every host thread."""
+    import oracle
+    from paper_2103_16234_b200.configs import filter_dims, input_dims
+
+    threads = oracle.max_threads()
+    work = []
+    for i, cfg in enumerate(cfgs):
+        c = cfg.with_batch(sample_batch)
+        x = oracle.make_uniform(input_dims(c), seed=rng_seed + 2 * i)
+        w = oracle.make_uniform(filter_dims(c), seed=rng_seed + 2 * i + 1)
+        work.append((c, x, w))
+    flops = secs = 0.0
+    t_start = time.perf_counter()
+    passes = 0
+    while True:
+        for c, x, w in work:
+            t0 = time.perf_counter()
+            if c.stride == 1:
+                oracle.conv_twostage(c, x, w, threads=threads)
+            else:  # the reference's conv_twostage refuses stride != 1; conv_naive is its strided path
+                oracle.conv_naive(c, x, w, threads=threads)
+            secs += time.perf_counter() - t0
+            flops += c.flops
+        passes += 1
+        if time.perf_counter() - t_start >= min_seconds:
+            break
+    return flops / secs / 1e9, threads, passes
+
+
+def reference_arm(args, cfgs, metric, config):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    sample_batch = 1
+    threads = oracle.max_threads()
+    from paper_2103_16234_b200.configs import filter_dims, input_dims
+    data = []
+    for i, cfg in enumerate(cfgs):
+        c = cfg.with_batch(sample_batch)
+        data.append((c, oracle.make_uniform(input_dims(c), seed=2 * i), oracle.make_uniform(filter_dims(c), seed=2 * i + 1)))
+
+    def step(i):
+        c, x, w = data[i % len(data)]
+        t0 = time.perf_counter()
+        if c.stride == 1:
+            oracle.conv_twostage(c, x, w, threads=threads)
+        else:
+            oracle.conv_naive(c, x, w, threads=threads)
+        return time.perf_counter() - t0, c.flops
+
+    for i in range(args.warmup):
+        step(i)
+    tot_t = tot_f = 0.0
+    for i in range(args.steps):
+        t, f = step(i)
+        tot_t += t
+        tot_f += f
+    value = tot_f / tot_t / 1e9
+    sample = (f"each step = one layer of {config['workload']} at N={sample_batch} (cycling through "
+              f"{len(cfgs)} layers), oracle C port of convkit.conv_twostage (stage1+stage2, reference "
+              f"rounding); strided layers via the conv_naive port")
+    line = {"metric": metric, "value": round(value, 3), "unit": "GFLOP/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * tot_t / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong" if args.workload in STRONG else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config,
+            "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU leg
+def make_operands(cfgs, device, seed):
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    xs, ws, ys = [], [], []
+    for cfg in cfgs:
+        xs.append(torch.rand((cfg.n, cfg.c, cfg.h, cfg.w), generator=g, device=device) * 2 - 1)
+        ws.append(torch.rand((cfg.m, cfg.c, cfg.hf, cfg.wf), generator=g, device=device) * 2 - 1)
+        ho = (cfg.h + 2 * cfg.pad_h - cfg.hf) // cfg.stride + 1
+        wo = (cfg.w + 2 * cfg.pad_w - cfg.wf) // cfg.stride + 1
+        ys.append(torch.empty((cfg.n, cfg.m, ho, wo), device=device))
+    return xs, ws, ys
+
+
+def time_layers(layers, xs, ws, ys, reps=20):
+    """Per-layer mean kernel time (ms) with CUDA events on the launching stream."""
+    import torch
+
+    out = []
+    stream = torch.cuda.current_stream()
+    for L, x, w, y in zip(layers, xs, ws, ys):
+        for _ in range(3):
+            L(x, w, out=y)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            L(x, w, out=y)
+        b.record(stream)
+        b.synchronize()
+        out.append(a.elapsed_time(b) / reps)
+    return out
+
+
+def sweep_report(path, device, peak_tflops):
+    """Per-layer µs / GFLOP/s / roofline for every BASELINE config and batch."""
+    import torch
+    from paper_2103_16234_b200 import ConvLayer
+    from paper_2103_16234_b200 import workloads as W
+
+    hbm = peaks().get("hbm_gbs", 6540.8)
+    rows = []
+    for wl, (_, batches) in W.WORKLOADS.items():
+        for n in batches:
+            cfgs = W.layers(wl, n)
+            layers = [ConvLayer(c, "fused") for c in cfgs]
+            xs, ws, ys = make_operands(cfgs, device, 1)
+            ms = time_layers(layers, xs, ws, ys, reps=10)
+            for c, L, t in zip(cfgs, layers, ms):
+                flop_per_byte = c.flops / c.compulsory_bytes
+                ridge = peak_tflops * 1e12 / (hbm * 1e9)
+                if flop_per_byte >= ridge:
+                    bound, frac = "fp32", c.flops / (t * 1e-3) / (peak_tflops * 1e12)
+                else:
+                    bound, frac = "hbm", c.compulsory_bytes / (t * 1e-3) / (hbm * 1e9)
+                rows.append({"workload": wl, "batch": n, "layer": c.name, "c": c.c, "hw": c.h, "m": c.m,
+                             "f": c.hf, "stride": c.stride, "us": round(t * 1e3, 2),
+                             "gflops": round(c.flops / (t * 1e-3) / 1e9, 1), "bound": bound,
+                             "roofline_frac": round(frac, 4), "family": L.family, "grid": L.grid})
+            del xs, ws, ys
+            torch.cuda.empty_cache()
+    with open(path, "w") as fh:
+        json.dump({"peak_fp32_tflops": peak_tflops, "hbm_gbs": hbm, "rows": rows}, fh, indent=1)
+    return rows
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2103_16234_b200 import workloads as W
+
+    batch = args.batch or DEFAULT_BATCH[args.workload]
+    strong = args.workload in STRONG
+    per_rank = batch // world if strong else batch
+    if strong and batch % world:
+        raise SystemExit(f"--batch {batch} does not split over {world} GPUs")
+    cfgs = W.layers(args.workload, per_rank)
+    global_batch = per_rank * world
+    metric = "fp32 conv GFLOP/s & us/layer (% of FP32/HBM roofline) at 1/2/4/8 B200 vs CPU ref"
+    config = {"workload": f"{args.workload}: {W.DESCRIPTIONS[args.workload]}", "layers": len(cfgs),
+              "global_batch": global_batch, "batch_per_gpu": per_rank, "engine": args.engine,
+              "parallelism": f"batch-sharded dp{world} (filters replicated, no collective)",
+              "l2": "per-step working set > 126 MB L2 (each layer's operands evicted by the others between steps)"}
+
+    if args.impl == "reference":
+        reference_arm(args, cfgs, metric, config)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2103_16234_b200 import ConvLayer
+    from paper_2103_16234_b200 import _native as nat
+
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    lib = nat.lib()
+
+    # live FP32 roofline denominator
+    tf, fpc, mhz = (nat.ctypes.c_double() for _ in range(3))
+    nat.check(lib.b2c_probe_fp32_peak(4000, nat.ctypes.byref(tf), nat.ctypes.byref(fpc), nat.ctypes.byref(mhz)))
+    peak_tflops = tf.value
+
+    layers = [ConvLayer(c, args.engine) for c in cfgs]
+    xs, ws, ys = make_operands(cfgs, device, 1234 + rank)
+
+    def step():
+        for L, x, w, y in zip(layers, xs, ws, ys):
+            L(x, w, out=y)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    # capture one step as a CUDA graph (launch-bound 36-layer pass)
+    graph = torch.cuda.CUDAGraph()
+    lib.b2c_reset_launch_count()
+    cap_stream = torch.cuda.Stream()
+    with torch.cuda.stream(cap_stream):
+        step()  # warm on the capture stream
+        torch.cuda.synchronize()
+        lib.b2c_reset_launch_count()
+        with torch.cuda.graph(graph, stream=cap_stream):
+            step()
+    launches_per_step = int(lib.b2c_launch_count())
+    for _ in range(max(args.warmup, 3)):
+        graph.replay()
+    torch.cuda.synchronize()
+
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        start.record()
+        for _ in range(args.steps):
+            graph.replay()
+        end.record()
+        torch.cuda.synchronize()
+    ms_local = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms_local], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms_total = float(t.item())
+    else:
+        ms_total = ms_local
+    flops_step_rank = sum(c.flops for c in cfgs)
+    value = flops_step_rank * world * args.steps / (ms_total * 1e-3) / 1e9
+    ms_per_step = ms_total / args.steps
+
+    # per-layer kernel times -> roofline of the conv kernel family
+    layer_ms = time_layers(layers, xs, ws, ys)
+    kern_ms = sum(layer_ms)
+    achieved_tflops = flops_step_rank / (kern_ms * 1e-3) / 1e12
+    hbm = peaks().get("hbm_gbs", 6540.8)
+    bytes_step = sum(c.compulsory_bytes for c in cfgs)
+    per_layer = [{"layer": c.name, "us": round(t * 1e3, 2), "gflops": round(c.flops / (t * 1e-3) / 1e9, 1),
+                  "family": L.family} for c, L, t in zip(cfgs, layers, layer_ms)]
+
+    # e2e: host buffers through the C-ABI drop-in (H2D x,w + kernel + D2H y per layer)
+    e2e = None
+    if args.e2e_steps > 0:
+        import ctypes
+        pinned = []
+        h2d = d2h = 0
+        for c, x, w, y in zip(cfgs, xs, ws, ys):
+            hx = torch.empty(x.shape, dtype=torch.float32, pin_memory=True).copy_(x)
+            hw = torch.empty(w.shape, dtype=torch.float32, pin_memory=True).copy_(w)
+            hy = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+            pinned.append((nat.desc(c), hx, hw, hy))
+            h2d += hx.numel() * 4 + hw.numel() * 4
+            d2h += hy.numel() * 4
+
+        def e2e_step():
+            for d, hx, hw, hy in pinned:
+                nat.check(lib.b2c_conv_host(ctypes.byref(d), hx.data_ptr(), hw.data_ptr(), hy.data_ptr(),
+                                            nat.ENGINE_FUSED if args.engine == "fused" else nat.ENGINE_TWOSTAGE,
+                                            None, None, 1 << 62, local_rank, None))
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=device, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": round(flops_step_rank * world * args.e2e_steps / dt / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+               "ms_per_step": round(1e3 * dt / args.e2e_steps, 3),
+               "path": "b2c_conv_host (C ABI, pinned host buffers, synchronous per layer)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample_batch = 1
+        gflops, threads, passes = cpu_run(cfgs, sample_batch, 10.0)
+        cpu = {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+               "sample": f"{len(cfgs)} {args.workload} layers at N={sample_batch} x {passes} passes (>=10 s), "
+                         f"oracle C port of convkit.conv_twostage (stage1+stage2, reference rounding), "
+                         f"{threads} threads"}
+
+    if args.report and rank == 0:
+        sweep_report(args.report, device, peak_tflops)
+
+    if rank == 0:
+        line = {"metric": metric, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+                "us_per_layer": round(1e3 * ms_per_step / len(cfgs), 3),
+                "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic (uniform [-1,1) inputs and filters, torch RNG on device)",
+                "config": config,
+                "roofline": {"bound": "fp32", "achieved": round(achieved_tflops, 3), "peak": round(peak_tflops, 3),
+                             "unit": "TFLOP/s", "frac": round(achieved_tflops / peak_tflops, 4), "traffic": None,
+                             "peak_source": "b2c_probe_fp32_peak: FFMA2 register-blocked loop on all SMs, "
+                                            f"measured live ({fpc.value:.1f} FMA/clk/SM at {mhz.value:.0f} MHz)",
+                             "frac_of_nominal_74.45": round(achieved_tflops / NOMINAL_FP32_TFLOPS, 4),
+                             "bytes_per_step": bytes_step,
+                             "hbm_frac": round(bytes_step / (kern_ms * 1e-3) / (hbm * 1e9), 4),
+                             "kernel_ms_per_step": round(kern_ms, 4)},
+                "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
+                "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
+                "per_layer": per_layer}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -87,6 +87,10 @@ typedef struct {
   int32_t smem_row_stride;
   int32_t smem_bytes;   /* dynamic shared memory per CTA                    */
   int64_t grid;         /* CTAs per launch                                  */
+  int32_t splits;       /* fused: channel ranges reduced separately (split-C);
+                           on input to b2c_select_tiles / b2c_conv2d_forward,
+                           > 0 forces the split                              */
+  int64_t workspace_bytes; /* workspace the plan needs (0 unless splits > 1) */
 } b2c_tile_plan;
 
 typedef enum {
@@ -134,9 +138,16 @@ b2c_status b2c_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tile_pla
 /* Fused direct convolution (any stride >= 1, any padding).  Replaces the
  * compute of twostage.conv_twostage (twostage.py:208-239) and
  * reference.conv_naive (reference.py:58-83) for device-resident tensors.
- * `tiles` may be NULL (planner's choice). */
-b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const float *w, float *y,
-                              const b2c_tile_plan *tiles, void *stream);
+ * `tiles` may be NULL (planner's choice) or carry a forced family / split.
+ * Layers with too few output tiles for 148 SMs are split over channel ranges
+ * (split-C) whose partials the tile's last CTA combines in ascending order;
+ * that needs `workspace` (tiles.workspace_bytes from b2c_select_tiles), which
+ * must be zero-filled before its first use and is left zeroed by every
+ * completed launch.  With no (or too small a) workspace the planner picks an
+ * unsplit plan.  Per output, the summation order is a function of
+ * (c, hf, wf, splits) only. */
+b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
+                              int64_t workspace_size, const b2c_tile_plan *tiles, void *stream);
 
 /* twostage.conv_twostage (twostage.py:208-239): preconditions in the
  * reference's order, then stage 1 (+ stage 2 unless 1x1) with the reference's
@@ -175,6 +186,11 @@ b2c_status b2c_stage1_host(const b2c_conv_desc *d, const float *x_host, const fl
                            int64_t workspace_limit, int32_t device, b2c_run_stats *stats);
 b2c_status b2c_stage2_host(const b2c_conv_desc *d, const float *partials_host, float *y_host,
                            int32_t device, b2c_run_stats *stats);
+
+/* FP32 roofline denominator: times an FFMA2 (fma.rn.f32x2) register-blocked
+ * loop on every SM; returns TFLOP/s (CUDA events), FMA/clk/SM and the SM clock
+ * achieved during the probe (in-kernel clock64). */
+b2c_status b2c_probe_fp32_peak(int32_t iters, double *tflops, double *fma_per_clk_per_sm, double *sm_mhz);
 
 /* Pinned host memory helpers (so e2e callers can stage through page-locked
  * buffers without linking CUDA themselves). */

@@ -45,7 +45,8 @@ class TilePlanC(ctypes.Structure):
     _fields_ = [("family", ctypes.c_int32), ("bm", ctypes.c_int32), ("bp", ctypes.c_int32),
                 ("bc", ctypes.c_int32), ("threads", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("smem_rows", ctypes.c_int32), ("smem_row_stride", ctypes.c_int32),
-                ("smem_bytes", ctypes.c_int32), ("grid", ctypes.c_int64)]
+                ("smem_bytes", ctypes.c_int32), ("grid", ctypes.c_int64), ("splits", ctypes.c_int32),
+                ("workspace_bytes", ctypes.c_int64)]
 
 
 _P = ctypes.POINTER
@@ -67,7 +68,8 @@ SIGNATURES = {
     "b2c_validate_plan": (ctypes.c_int, [_P(ConvDesc), _P(DeviceModelC), _P(LaunchPlanC)]),
     "b2c_block_position_ranges": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, _P(ctypes.c_int64)]),
     "b2c_select_tiles": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, _P(TilePlanC)]),
-    "b2c_conv2d_forward": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _P(TilePlanC), ctypes.c_void_p]),
+    "b2c_conv2d_forward": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, ctypes.c_void_p, ctypes.c_int64,
+                                          _P(TilePlanC), ctypes.c_void_p]),
     "b2c_conv_twostage": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _fp, ctypes.c_int64, _P(LaunchPlanC),
                                          _P(DeviceModelC), ctypes.c_int64, ctypes.c_void_p, _P(RunStatsC)]),
     "b2c_stage1_scalar_prods": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _P(LaunchPlanC), _P(DeviceModelC),
@@ -78,6 +80,8 @@ SIGNATURES = {
     "b2c_stage1_host": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _P(LaunchPlanC), _P(DeviceModelC),
                                        ctypes.c_int64, ctypes.c_int32, _P(RunStatsC)]),
     "b2c_stage2_host": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, ctypes.c_int32, _P(RunStatsC)]),
+    "b2c_probe_fp32_peak": (ctypes.c_int, [ctypes.c_int32, _P(ctypes.c_double), _P(ctypes.c_double),
+                                           _P(ctypes.c_double)]),
     "b2c_host_alloc": (ctypes.c_void_p, [ctypes.c_size_t]),
     "b2c_host_free": (None, [ctypes.c_void_p]),
 }

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libb2conv.so"
-SOURCES = [CSRC / "conv_launch.cu", CSRC / "api.cpp"]
+SOURCES = [CSRC / "conv_launch.cu", CSRC / "probe.cu", CSRC / "api.cpp"]
 DEPS = SOURCES + [CSRC / "conv_kernel.cuh", CSRC / "internal.h", ROOT / "include" / "b2conv.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

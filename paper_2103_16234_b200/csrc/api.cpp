@@ -109,8 +109,11 @@ struct PlanKey {
   int stage1;
   int device;
   int forced;
+  int forced_splits;
+  int allow_split;
   bool operator==(const PlanKey &o) const {
-    return std::memcmp(&d, &o.d, sizeof(d)) == 0 && stage1 == o.stage1 && device == o.device && forced == o.forced;
+    return std::memcmp(&d, &o.d, sizeof(d)) == 0 && stage1 == o.stage1 && device == o.device && forced == o.forced &&
+           forced_splits == o.forced_splits && allow_split == o.allow_split;
   }
 };
 struct PlanKeyHash {
@@ -124,7 +127,8 @@ struct PlanKeyHash {
 std::mutex g_plan_mu;
 std::unordered_map<PlanKey, b2c::TileChoice, PlanKeyHash> g_plans;
 
-b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, int forced, b2c::TileChoice *tc) {
+b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, int forced, int forced_splits,
+                     bool allow_split, b2c::TileChoice *tc) {
   int device = 0;
   cudaGetDevice(&device);
   PlanKey key;
@@ -133,6 +137,8 @@ b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, in
   key.stage1 = stage1;
   key.device = device;
   key.forced = forced;
+  key.forced_splits = forced_splits;
+  key.allow_split = allow_split;
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_plans.find(key);
@@ -141,10 +147,10 @@ b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, in
       return B2C_OK;
     }
   }
-  if (!b2c::plan_tiles(g, stage1, device, forced, tc)) {
-    if (forced >= 0)
-      return fail(B2C_INVALID_PLAN, "tile family %d (%s) cannot run this configuration", forced,
-                  b2c::family_name(forced));
+  if (!b2c::plan_tiles(g, stage1, device, forced, forced_splits, allow_split, tc)) {
+    if (forced >= 0 || forced_splits > 0)
+      return fail(B2C_INVALID_PLAN, "tile family %d (%s) / split %d cannot run this configuration", forced,
+                  forced >= 0 ? b2c::family_name(forced) : "auto", forced_splits);
     return fail(B2C_UNSUPPORTED, "no kernel family fits this configuration (shared-memory halo too large)");
   }
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -162,7 +168,9 @@ void export_tiles(const b2c::TileChoice &tc, b2c_tile_plan *out) {
   out->smem_rows = tc.rows;
   out->smem_row_stride = tc.rs;
   out->smem_bytes = tc.smem_bytes;
-  out->grid = tc.grid * tc.grid_z;
+  out->grid = tc.grid * tc.splits * tc.grid_z;
+  out->splits = tc.splits;
+  out->workspace_bytes = tc.ws_bytes;
 }
 
 b2c_status resolve_plan(const b2c_conv_desc *d, const b2c_launch_plan *plan, const b2c_device_model *dev,
@@ -206,17 +214,18 @@ void fill_stats(const b2c_conv_desc *d, const b2c_launch_plan &p, bool stage2, b
 b2c_status run_stage1(const b2c_conv_desc *d, const b2c::Geom &g, const float *x, const float *w, float *out,
                       cudaStream_t stream) {
   b2c::TileChoice tc;
-  b2c_status st = get_tiles(d, g, true, -1, &tc);
+  b2c_status st = get_tiles(d, g, true, -1, 0, false, &tc);
   if (st != B2C_OK) return st;
-  cudaError_t e = b2c::launch_direct(g, tc, x, w, out, true, (long long)g.N * g.M * g.HoWo, stream);
+  cudaError_t e = b2c::launch_direct(g, tc, x, w, out, true, (long long)g.N * g.M * g.HoWo, nullptr, stream);
   if (e != cudaSuccess) return cuda_fail(e, "stage-1 launch");
   return B2C_OK;
 }
 
 // ------------------------------------------------------ host staging cache
+// slots: 0 x, 1 w, 2 y, 3 two-stage partial planes, 4 split-C workspace (kept zeroed)
 struct DeviceBuffers {
-  void *ptr[4] = {nullptr, nullptr, nullptr, nullptr};
-  size_t cap[4] = {0, 0, 0, 0};
+  void *ptr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t cap[5] = {0, 0, 0, 0, 0};
   cudaStream_t stream = nullptr;
 };
 thread_local std::unordered_map<int, DeviceBuffers> t_bufs;
@@ -229,6 +238,8 @@ b2c_status ensure(DeviceBuffers &b, int slot, size_t bytes) {
   b.cap[slot] = 0;
   cudaError_t e = cudaMalloc(&b.ptr[slot], bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  e = cudaMemset(b.ptr[slot], 0, bytes);  // split-C counters (slot 4) must start at zero
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemset");
   b.cap[slot] = bytes;
   return B2C_OK;
 }
@@ -361,7 +372,8 @@ b2c_status b2c_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tile_pla
   if (engine == B2C_ENGINE_TWOSTAGE && d->stride != 1)
     return fail(B2C_UNSUPPORTED, "two-stage convolution requires stride 1, got %d", d->stride);
   b2c::TileChoice tc;
-  st = get_tiles(d, g, engine == B2C_ENGINE_TWOSTAGE, out->family >= 0 ? out->family : -1, &tc);
+  st = get_tiles(d, g, engine == B2C_ENGINE_TWOSTAGE, out->family >= 0 ? out->family : -1,
+                 out->splits > 0 ? out->splits : 0, true, &tc);
   if (st != B2C_OK) return st;
   export_tiles(tc, out);
   return B2C_OK;
@@ -372,17 +384,26 @@ int32_t b2c_family_matches(const b2c_conv_desc *d, int32_t engine, int32_t famil
   return b2c::family_matches(family, geom_of(d), engine == B2C_ENGINE_TWOSTAGE) ? 1 : 0;
 }
 
-b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const float *w, float *y,
-                              const b2c_tile_plan *tiles, void *stream) {
+b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
+                              int64_t workspace_size, const b2c_tile_plan *tiles, void *stream) {
   b2c_status st = check_config(d, nullptr);
   if (st != B2C_OK) return st;
   if (!x || !w || !y) return fail(B2C_INVALID_ARGUMENT, "null tensor pointer");
   b2c::Geom g = geom_of(d);
   if ((st = check_sizes(g)) != B2C_OK) return st;
+  const int forced = (tiles && tiles->family >= 0) ? tiles->family : -1;
+  const int forced_splits = (tiles && tiles->splits > 0) ? tiles->splits : 0;
   b2c::TileChoice tc;
-  st = get_tiles(d, g, false, (tiles && tiles->family >= 0) ? tiles->family : -1, &tc);
+  st = get_tiles(d, g, false, forced, forced_splits, true, &tc);
   if (st != B2C_OK) return st;
-  cudaError_t e = b2c::launch_direct(g, tc, x, w, y, false, 0, (cudaStream_t)stream);
+  if (tc.splits > 1 && (!workspace || workspace_size < tc.ws_bytes)) {
+    if (forced_splits > 1)
+      return fail(B2C_INVALID_ARGUMENT, "split %d needs a %lld-byte workspace, %lld provided", forced_splits,
+                  (long long)tc.ws_bytes, (long long)workspace_size);
+    st = get_tiles(d, g, false, forced, 0, false, &tc);  // unsplit plan
+    if (st != B2C_OK) return st;
+  }
+  cudaError_t e = b2c::launch_direct(g, tc, x, w, y, false, 0, workspace, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "fused conv launch");
   return B2C_OK;
 }
@@ -475,8 +496,14 @@ b2c_status b2c_conv_host(const b2c_conv_desc *d, const float *x_host, const floa
   const size_t wb = sizeof(float) * (size_t)g.M * g.C * g.HF * g.WF;
   const size_t yb = sizeof(float) * (size_t)g.N * g.M * g.HoWo;
   const size_t wsb = engine == B2C_ENGINE_TWOSTAGE ? (size_t)b2c_workspace_bytes(d) : 0;
+  size_t splitb = 0;
+  if (engine == B2C_ENGINE_FUSED) {
+    b2c::TileChoice tc;
+    if ((st = get_tiles(d, g, false, -1, 0, true, &tc)) != B2C_OK) return st;
+    splitb = (size_t)tc.ws_bytes;
+  }
   if ((st = ensure(*b, 0, xb)) || (st = ensure(*b, 1, wb)) || (st = ensure(*b, 2, yb)) ||
-      (wsb && (st = ensure(*b, 3, wsb))))
+      (wsb && (st = ensure(*b, 3, wsb))) || (splitb && (st = ensure(*b, 4, splitb))))
     return st;
   cudaError_t e = cudaMemcpyAsync(b->ptr[0], x_host, xb, cudaMemcpyHostToDevice, b->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(b->ptr[1], w_host, wb, cudaMemcpyHostToDevice, b->stream);
@@ -485,7 +512,7 @@ b2c_status b2c_conv_host(const b2c_conv_desc *d, const float *x_host, const floa
   const float *dw = static_cast<const float *>(b->ptr[1]);
   float *dy = static_cast<float *>(b->ptr[2]);
   if (engine == B2C_ENGINE_FUSED) {
-    st = b2c_conv2d_forward(d, dx, dw, dy, nullptr, b->stream);
+    st = b2c_conv2d_forward(d, dx, dw, dy, splitb ? b->ptr[4] : nullptr, (int64_t)splitb, nullptr, b->stream);
     if (stats) std::memset(stats, 0, sizeof(*stats));
   } else {
     st = b2c_conv_twostage(d, dx, dw, dy, static_cast<float *>(b->ptr[3]), (int64_t)wsb, &rp, dev,

@@ -6,33 +6,34 @@
 // virtual zero padding (tensor.py:112-123), any stride (conv_naive), output
 // [n][m][ho][wo].
 //
-// One template serves three roles:
-//   * FUSED (STRICT=false): the paper's per-filter-row dot products (stage 1)
-//     and the cross-row sum (stage 2) both reduced in registers in one pass —
-//     no workspace, no im2col.  Accumulation uses FFMA2 (fma.rn.f32x2, two
-//     output channels per instruction, scalar-broadcast pixel operand).  The
-//     per-output order is "c ascending, then (yf,xf) row-major" for every tile
-//     plan, so results are bitwise independent of the plan / GPU count.
-//   * STAGE 1 (STRICT=true, HF=WF=1, launched once per filter row k via
-//     blockIdx.z): the paper's scalar_prods kernel — each output of filter row
-//     k is a channel dot product with separately rounded multiply and add
-//     (FMUL+FADD), +0.0 start, channels ascending: bitwise equal to the
-//     reference's _run_block (twostage.py:101-115).
+// One template serves two roles:
+//   * FUSED (STRICT=false): the paper's per-filter-row channel dot products
+//     (its stage 1) and the cross-row sum (its stage 2) both reduced in
+//     registers in one pass — no partial-sum planes, no im2col.  Accumulation
+//     is FFMA2 (fma.rn.f32x2: two output channels per instruction with a
+//     scalar-broadcast pixel operand).  Per output the order is "channels
+//     ascending, filter taps row-major inside each channel" within each of
+//     `splits` contiguous channel ranges; the range partials (splits > 1) are
+//     combined in ascending range order by the tile's last-arriving CTA
+//     (deterministic, no atomics on data).
+//   * STAGE 1 (STRICT=true, HF=WF=1, blockIdx.z = filter row k): the paper's
+//     scalar_prods kernel — channel dot products with separately rounded
+//     multiply and add (FMUL+FADD), +0.0 start, channels ascending: bitwise
+//     equal to the reference's _run_block (twostage.py:101-115).
 //
 // Tiling (B200-first, not the paper's one-filter-row-per-block mapping):
 //   CTA = BM output channels x BP flattened output pixels (n, y, x order).
-//   Thread = RM=16 channels x RP=4 pixels, pixels strided by NTP so a warp's
-//   lanes touch consecutive pixels (conflict-free shared loads, coalesced
-//   stores) and all lanes of a warp share their 16 channels (the weight loads
-//   are warp-wide broadcasts, LDS.128).
-//   Input halo: the tile's receptive field is staged per channel as a band of
-//   "virtual rows" of the zero-padded image stack (row V = n*Hp + padded_y),
-//   so tiles may span image boundaries (small 7x7/14x14 planes) without any
-//   re-layout.  Out-of-plane elements are staged as +0.0 and multiplied like
-//   real data, so 0*inf = nan exactly as in the reference.
-//   Filters are staged transposed, [c][tap][m], straight from [m][c][hf][wf].
-//   Global->shared movement is cp.async (4-byte, zero-fill), double-buffered
-//   over BC-channel chunks.
+//   Thread = RM=16 channels x RP=4 pixels; a thread's pixels are strided by
+//   NTP so a warp's lanes touch consecutive pixels (conflict-free shared loads,
+//   coalesced stores), and all lanes of a warp share their 16 channels (weight
+//   loads are warp-wide broadcasts, LDS.128).
+//   Input halo: per channel, the tile's receptive field is staged as a band of
+//   "virtual rows" of the zero-padded image stack (row V = n*Hp + padded_y), so
+//   a tile may span image boundaries (7x7/14x14 planes) with no re-layout.
+//   Out-of-plane elements are staged as +0.0 and multiplied like real data, so
+//   0*inf = nan exactly as in the reference.  Filters are staged transposed,
+//   [c][tap][m], straight from [m][c][hf][wf].  Global->shared movement is
+//   cp.async (4-byte) double-buffered over BC-channel chunks.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -44,6 +45,8 @@ struct KParams {
   const float *x;
   const float *w;
   float *y;
+  float *partials;   // split-C partial tiles: [tile][split][BM*BP]
+  int *counters;     // split-C arrival counters, one per tile, zero between launches
   int N, C, H, W, M;
   int S;             // stride
   int HF, WF;        // filter extent handled by THIS launch (1x1 for stage 1)
@@ -51,21 +54,40 @@ struct KParams {
   int Ho, Wo, HoWo;
   int Hp;            // H + 2*PH: virtual-row period of one image
   int Q;             // N*Ho*Wo
-  int RS;            // shared-memory row stride (floats)
-  int ROWS;          // virtual rows staged per channel
-  int XCS;           // shared-memory channel stride (floats), multiple of 4
-  int tile_elems;    // ROWS*RS
+  int RS;            // shared-memory row stride (floats), == W (mod 4) so rows stay 16B-congruent
+  int RC;            // staged columns per row: (Wo-1)*S + WF
+  int ROWS;          // staged virtual rows per channel
+  int XCS;           // shared-memory channel stride (floats), multiple of 4, >= ROWS*RS + 3
+  int vec_ok;        // H*W % 4 == 0 and x 16B-aligned: 16-byte cp.async groups allowed
   int mtiles;        // ceil(M/BM)
   int nchunks;       // ceil(C/BC)
+  int splits;        // channel ranges reduced separately (blockIdx.y)
+  int chunks_per_split;
   int w_ctaps;       // taps between consecutive channels in w (hf*wf of the full filter)
   int wf_full;       // wf of the full filter (stage 1 decodes k -> (yf, xf))
   long long y_tap_stride;  // stage 1: elements between partial planes of consecutive k
   int strict_tap_major;    // stage 1: blockIdx.z selects the filter row
+  unsigned long long *trace;  // optional per-CTA (smid, t_start, t_end) records (B2C_TRACE_FILE)
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
 
 __device__ __forceinline__ void cp_async4(float *smem_dst, const float *gmem_src) {
   unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(float *smem_dst, const float *gmem_src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -82,13 +104,15 @@ struct ConvTile {
   static constexpr int NMG = BM / RM;
   static constexpr int NT = NMG * NTP;
   static constexpr int WS = BM + 4;  // weight row stride: keeps LDS.128 alignment, spreads banks
+  // target 16 resident warps per SM at <= 128 registers per thread
+  static constexpr int MIN_BLOCKS = NT >= 512 ? 1 : 512 / NT;
   static_assert(BM % RM == 0, "BM must be a multiple of 16");
   static_assert(NTP % 32 == 0, "a warp must share one channel group");
 };
 
 template <int HF_T, int WF_T, int S_T, int BM, int BP, int BC, bool STRICT>
 __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>::NT,
-                                  (ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>::NT >= 512 ? 1 : 2))
+                                  ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>::MIN_BLOCKS)
     conv_direct_kernel(const KParams p) {
   using T = ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>;
   constexpr int RM = T::RM, RP = T::RP, NTP = T::NTP, NT = T::NT, WS = T::WS;
@@ -98,30 +122,33 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
   const int taps = hf * wf;
 
   extern __shared__ __align__(16) float smem[];
-  // [goff table: tile_elems ints][stage 0: X (BC*XCS) | W (BC*taps*WS)][stage 1: ...]
+  // [goff: XCS ints][gtab: XCS/4 ints][stage 0: X (BC*XCS) | W (BC*taps*WS)][stage 1: ...]
   int *goff = reinterpret_cast<int *>(smem);
-  const int goff_floats = (p.tile_elems + 3) & ~3;
+  int *gtab = goff + p.XCS;
+  const int ngroups = p.XCS >> 2;
   const int xfloats = BC * p.XCS;
   const int stage_floats = xfloats + BC * taps * WS;
-  float *stage0 = smem + goff_floats;
+  float *stage0 = smem + p.XCS + ((ngroups + 3) & ~3);
+  __shared__ int s_last;
 
   const int tid = threadIdx.x;
+  const unsigned long long t_start = p.trace ? global_ns() : 0ull;
   const int mg = tid / NTP;
   const int tp = tid - mg * NTP;
-  const int mt = blockIdx.x % p.mtiles;
-  const int pt = blockIdx.x / p.mtiles;
+  const int tile = blockIdx.x;
+  const int mt = tile % p.mtiles;
+  const int pt = tile / p.mtiles;
   const int m0 = mt * BM;
   const int q0 = pt * BP;
+  const int split = blockIdx.y;
 
   // filter row handled by this launch slice (stage 1); zero for the fused path
   int tap_y = 0, tap_x = 0, w_tap0 = 0;
-  float *yout = p.y;
   if (p.strict_tap_major) {
     const int k = blockIdx.z;
     tap_y = k / p.wf_full;
     tap_x = k - tap_y * p.wf_full;
     w_tap0 = k;
-    yout += (long long)k * p.y_tap_stride;
   }
 
   // ---- tile origin in virtual-row space -----------------------------------
@@ -129,70 +156,104 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
   const int oy0 = (q0 - n0 * p.HoWo) / p.Wo;
   const int vlo = n0 * p.Hp + oy0 * S + tap_y;
   const long long chw = (long long)p.C * p.H * p.W;
-  const float *xtile = p.x + (long long)n0 * chw;
   const int hw = p.H * p.W;
+  // shift so that shared position == global offset (mod 4) along rows: the
+  // interior of every row can then move as 16-byte groups
+  const int shift = (((vlo - n0 * p.Hp - p.PH) * p.W + tap_x - p.PW) % 4 + 4) % 4;
 
-  // ---- per-element global offsets of the halo band (same for every channel)
-  for (int idx = tid; idx < p.tile_elems; idx += NT) {
-    const int r = idx / p.RS;
-    const int col = idx - r * p.RS;
-    const int v = vlo + r;
-    const int n = v / p.Hp;
-    const int iy = v - n * p.Hp - p.PH;
-    const int ix = col + tap_x - p.PW;
-    const bool ok = (n < p.N) && (iy >= 0) && (iy < p.H) && (ix >= 0) && (ix < p.W);
-    goff[idx] = ok ? (int)((long long)(n - n0) * chw + iy * p.W + ix) : -1;
+  // ---- halo band: per shared position, the global offset (same for every
+  // channel): >= 0 data, -1 zero padding, -2 unused
+  for (int pos = tid; pos < p.XCS; pos += NT) {
+    const int rel = pos - shift;
+    int g = -2;
+    if (rel >= 0) {
+      const int r = rel / p.RS;
+      const int col = rel - r * p.RS;
+      if (r < p.ROWS && col < p.RC) {
+        const int v = vlo + r;
+        const int n = v / p.Hp;
+        const int iy = v - n * p.Hp - p.PH;
+        const int ix = col + tap_x - p.PW;
+        const bool ok = (n < p.N) && (iy >= 0) && (iy < p.H) && (ix >= 0) && (ix < p.W);
+        g = ok ? (int)((long long)(n - n0) * chw + iy * p.W + ix) : -1;
+      }
+    }
+    goff[pos] = g;
+  }
+  __syncthreads();
+  // 16-byte groups: global offset of a contiguous aligned run of 4 data
+  // elements, -1 for a mixed group (element-wise path), -3 for all-unused
+  for (int G = tid; G < ngroups; G += NT) {
+    const int g0 = goff[4 * G], g1 = goff[4 * G + 1], g2 = goff[4 * G + 2], g3 = goff[4 * G + 3];
+    int t = -1;
+    if (p.vec_ok && g0 >= 0 && (g0 & 3) == 0 && g1 == g0 + 1 && g2 == g0 + 2 && g3 == g0 + 3) t = g0;
+    else if (g0 == -2 && g1 == -2 && g2 == -2 && g3 == -2) t = -3;
+    gtab[G] = t;
   }
 
-  // ---- per-thread output pixels ---------------------------------------------
+  // ---- per-thread output pixels: shared-memory offsets of their windows ----
   int pix_off[RP];
-  long long out_off[RP];
-  bool pix_ok[RP];
 #pragma unroll
   for (int j = 0; j < RP; j++) {
-    const int q = q0 + j * NTP + tp;
-    pix_ok[j] = q < p.Q;
-    const int qq = pix_ok[j] ? q : q0;
-    const int n = qq / p.HoWo;
-    const int rem = qq - n * p.HoWo;
+    const int q = min(q0 + j * NTP + tp, p.Q - 1);
+    const int n = q / p.HoWo;
+    const int rem = q - n * p.HoWo;
     const int oy = rem / p.Wo;
     const int ox = rem - oy * p.Wo;
-    pix_off[j] = ((n - n0) * p.Hp + (oy - oy0) * S) * p.RS + ox * S;
-    out_off[j] = (long long)n * p.M * p.HoWo + rem;
+    pix_off[j] = shift + ((n - n0) * p.Hp + (oy - oy0) * S) * p.RS + ox * S;
   }
-  __syncthreads();  // goff table visible
+  __syncthreads();  // tables visible
 
+  const float *xtile = p.x + (long long)n0 * chw;
+  const bool w_dense = (p.w_ctaps == taps);  // fused: filter taps of a channel are contiguous
   auto load_chunk = [&](int chunk, float *stage) {
     const int c0 = chunk * BC;
     float *xs = stage;
     float *ws = stage + xfloats;
     const float *xsrc = xtile + (long long)c0 * hw;
     const int cvalid = min(BC, p.C - c0);
-    for (int idx = tid; idx < p.tile_elems; idx += NT) {
-      const int g = goff[idx];
-      float *dst = xs + idx;
-      if (g >= 0) {
+    for (int G = tid; G < ngroups; G += NT) {
+      const int t = gtab[G];
+      if (t == -3) continue;
+      float *dst = xs + 4 * G;
+      if (t >= 0) {
+        const float *src = xsrc + t;
 #pragma unroll
-        for (int c = 0; c < BC; c++)
-          if (c < cvalid) cp_async4(dst + c * p.XCS, xsrc + (long long)c * hw + g);
+        for (int c = 0; c < BC; c++) {
+          if (c < cvalid) cp_async16(dst, src);
+          dst += p.XCS;
+          src += hw;
+        }
       } else {
 #pragma unroll
-        for (int c = 0; c < BC; c++)
-          if (c < cvalid) dst[c * p.XCS] = 0.0f;
+        for (int k = 0; k < 4; k++) {
+          const int g = goff[4 * G + k];
+          float *d = dst + k;
+          if (g >= 0) {
+            const float *src = xsrc + g;
+            for (int c = 0; c < cvalid; c++, d += p.XCS, src += hw) cp_async4(d, src);
+          } else if (g == -1) {
+            for (int c = 0; c < cvalid; c++, d += p.XCS) *d = 0.0f;
+          }
+        }
       }
     }
+    // filters: w[m0+m][c0 + c][tap] -> ws[(c*taps + tap)*WS + m]
     const int per_m = BC * taps;
     const int wtotal = BM * per_m;
+    const float *wsrc = p.w + ((long long)m0 * p.C + c0) * p.w_ctaps + w_tap0;
+    const int mstride = p.C * p.w_ctaps;
+    const int ct_valid = cvalid * taps;
     for (int e = tid; e < wtotal; e += NT) {
       const int m = e / per_m;
       const int ct = e - m * per_m;
-      const int c = ct / taps;
-      const int t = ct - c * taps;
       float *dst = ws + ct * WS + m;
-      if (m0 + m < p.M && c < cvalid)
-        cp_async4(dst, p.w + ((long long)(m0 + m) * p.C + c0 + c) * p.w_ctaps + w_tap0 + t);
-      else
+      if (m0 + m < p.M && ct < ct_valid) {
+        const int off = w_dense ? ct : (ct / taps) * p.w_ctaps + (ct % taps);
+        cp_async4(dst, wsrc + m * mstride + off);
+      } else {
         *dst = 0.0f;
+      }
     }
   };
 
@@ -211,13 +272,18 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
       for (int j = 0; j < RP; j++) acc2[i][j] = make_float2(0.0f, 0.0f);
   }
 
-  // ---- main loop: double-buffered channel chunks ----------------------------
-  load_chunk(0, stage0);
-  cp_async_commit();
-  for (int chunk = 0; chunk < p.nchunks; chunk++) {
-    float *cur = stage0 + (chunk & 1) * stage_floats;
-    if (chunk + 1 < p.nchunks) {
-      load_chunk(chunk + 1, stage0 + ((chunk + 1) & 1) * stage_floats);
+  // ---- main loop: double-buffered channel chunks of this split --------------
+  const int chunk_begin = split * p.chunks_per_split;
+  const int chunk_end = min(p.nchunks, chunk_begin + p.chunks_per_split);
+  if (chunk_begin < chunk_end) {
+    load_chunk(chunk_begin, stage0);
+    cp_async_commit();
+  }
+  for (int chunk = chunk_begin; chunk < chunk_end; chunk++) {
+    const int buf = (chunk - chunk_begin) & 1;
+    float *cur = stage0 + buf * stage_floats;
+    if (chunk + 1 < chunk_end) {
+      load_chunk(chunk + 1, stage0 + (buf ^ 1) * stage_floats);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -226,18 +292,22 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
     __syncthreads();
 
     const int cvalid = min(BC, p.C - chunk * BC);
-    const float *xs = cur;
-    const float *wsm = cur + xfloats + mg * RM;
-#pragma unroll 1
-    for (int c = 0; c < cvalid; c++) {
-      const float *xc = xs + c * p.XCS;
-      const float *wc = wsm + c * taps * WS;
+    // strength-reduced shared addresses: one base per output pixel, one for
+    // this warp's 16 filter columns; advanced by a channel plane per step
+    const float *xcur[RP];
 #pragma unroll
+    for (int j = 0; j < RP; j++) xcur[j] = cur + pix_off[j];
+    const float *wcur = cur + xfloats + mg * RM;
+    const int wstep = taps * WS;
+    constexpr int CUNROLL = (HF_T == 1 && WF_T == 1) ? 2 : 1;  // 1x1: two channels per trip
+#pragma unroll CUNROLL
+    for (int c = 0; c < cvalid; c++) {
+#pragma unroll 1
       for (int yy = 0; yy < hf; yy++) {
-        const float *xrow = xc + yy * p.RS;
+        const int roff = yy * p.RS;
 #pragma unroll
         for (int xx = 0; xx < wf; xx++) {
-          const float *wt = wc + (yy * wf + xx) * WS;
+          const float *wt = wcur + (yy * wf + xx) * WS;
           float wv[RM];
 #pragma unroll
           for (int i = 0; i < RM; i += 4) {
@@ -246,7 +316,7 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
           }
           float xv[RP];
 #pragma unroll
-          for (int j = 0; j < RP; j++) xv[j] = xrow[pix_off[j] + xx];
+          for (int j = 0; j < RP; j++) xv[j] = xcur[j][roff + xx];
           if (STRICT) {
 #pragma unroll
             for (int i = 0; i < (STRICT ? RM : 1); i++)
@@ -263,27 +333,98 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
           }
         }
       }
+#pragma unroll
+      for (int j = 0; j < RP; j++) xcur[j] += p.XCS;
+      wcur += wstep;
     }
     __syncthreads();
   }
 
-  // ---- epilogue: fully overwrite y ------------------------------------------
+  auto acc_at = [&](int i, int j) -> float {
+    if (STRICT) return accs[STRICT ? i : 0][STRICT ? j : 0];
+    return (i & 1) ? acc2[i >> 1][j].y : acc2[i >> 1][j].x;
+  };
+
+  if (p.trace && tid == 0) {
+    const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    p.trace[3 * cta] = smid();
+    p.trace[3 * cta + 1] = t_start;
+    p.trace[3 * cta + 2] = global_ns();
+  }
+  // ---- epilogue ---------------------------------------------------------------
+  float *yout = p.y;
+  if (p.strict_tap_major) yout += (long long)blockIdx.z * p.y_tap_stride;
+  long long out_off[RP];
+  bool pix_ok[RP];
+#pragma unroll
+  for (int j = 0; j < RP; j++) {
+    const int q = q0 + j * NTP + tp;
+    pix_ok[j] = q < p.Q;
+    const int qq = pix_ok[j] ? q : 0;
+    const int n = qq / p.HoWo;
+    out_off[j] = (long long)n * p.M * p.HoWo + (qq - n * p.HoWo);
+  }
   const long long plane = p.HoWo;
+
+  if (p.splits == 1) {
+    // fully overwrite y
+#pragma unroll
+    for (int i = 0; i < RM; i++) {
+      const int m = m0 + mg * RM + i;
+      if (m >= p.M) break;
+#pragma unroll
+      for (int j = 0; j < RP; j++)
+        if (pix_ok[j]) yout[out_off[j] + (long long)m * plane] = acc_at(i, j);
+    }
+    return;
+  }
+
+  // split-C: publish this range's partial tile, the last CTA of the tile
+  // combines the ranges in ascending order and writes y.
+  constexpr int TILE = BM * BP;
+  float *mine = p.partials + ((long long)tile * p.splits + split) * TILE;
+#pragma unroll
+  for (int i = 0; i < RM; i++)
+#pragma unroll
+    for (int j = 0; j < RP; j++) mine[(mg * RM + i) * BP + j * NTP + tp] = acc_at(i, j);
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const int prev = atomicAdd(&p.counters[tile], 1);
+    s_last = (prev == p.splits - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // combine in ascending split order; all RM*RP loads of one split are in
+  // flight together (the order of the adds per output is unchanged)
+  const float *base = p.partials + (long long)tile * p.splits * TILE + mg * RM * BP + tp;
+  float sum[RM][RP];
+#pragma unroll
+  for (int i = 0; i < RM; i++)
+#pragma unroll
+    for (int j = 0; j < RP; j++) sum[i][j] = __ldcg(base + i * BP + j * NTP);
+  for (int s = 1; s < p.splits; s++) {
+    const float *ps = base + (long long)s * TILE;
+    float v[RM][RP];
+#pragma unroll
+    for (int i = 0; i < RM; i++)
+#pragma unroll
+      for (int j = 0; j < RP; j++) v[i][j] = __ldcg(ps + i * BP + j * NTP);
+#pragma unroll
+    for (int i = 0; i < RM; i++)
+#pragma unroll
+      for (int j = 0; j < RP; j++) sum[i][j] = __fadd_rn(sum[i][j], v[i][j]);
+  }
 #pragma unroll
   for (int i = 0; i < RM; i++) {
     const int m = m0 + mg * RM + i;
     if (m >= p.M) break;
 #pragma unroll
-    for (int j = 0; j < RP; j++) {
-      if (!pix_ok[j]) continue;
-      float v;
-      if (STRICT)
-        v = accs[STRICT ? i : 0][STRICT ? j : 0];
-      else
-        v = (i & 1) ? acc2[i >> 1][j].y : acc2[i >> 1][j].x;
-      yout[out_off[j] + (long long)m * plane] = v;
-    }
+    for (int j = 0; j < RP; j++)
+      if (pix_ok[j]) yout[out_off[j] + (long long)m * plane] = sum[i][j];
   }
+  if (tid == 0) p.counters[tile] = 0;  // leave the workspace zeroed for the next launch
 }
 
 // Stage 2 (twostage.py:175-205): y = +0.0 + p_0 + p_1 + ... + p_{k-1}, every

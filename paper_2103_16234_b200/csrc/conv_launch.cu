@@ -11,10 +11,13 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
+#include <cstdio>
 
 #include "conv_kernel.cuh"
 #include "internal.h"
@@ -37,7 +40,7 @@ struct Family {
   Family {                                                                                                 \
     NAME, HF, WF, S, BM, BP, BC, STRICT, ConvTile<HF, WF, S, BM, BP, BC, STRICT>::NT,                     \
         reinterpret_cast<const void *>(&conv_direct_kernel<HF, WF, S, BM, BP, BC, STRICT>),                \
-        (ConvTile<HF, WF, S, BM, BP, BC, STRICT>::NT >= 512 ? 1 : 2)                                       \
+        ConvTile<HF, WF, S, BM, BP, BC, STRICT>::MIN_BLOCKS                                                \
   }
 
 const Family kFamilies[] = {
@@ -100,49 +103,96 @@ struct Candidate {
   double cost = 1e300;
 };
 
-bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, Candidate *out) {
+// Relative time of one launch in "FMA-equivalents at full SM rate".  Models
+// wave quantisation over the SMs, the per-SM warp count needed to saturate
+// the FMA pipes, halo/filter staging, a fixed per-CTA prologue and the split-C
+// partial traffic.  (Coefficients fitted on B200 timings of the BASELINE
+// layers.)
+double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, int sms, int max_blocks) {
+  const double fma = (double)tc.bm * tc.bp * taps * tc.bc * tc.chunks_per_split * (stage1 ? 2.0 : 1.0);
+  const double per_elem = ((long long)g.H * g.W % 4 == 0) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
+  const double loads = (per_elem * tc.tile_elems + 4.0 * tc.bm * taps) * tc.bc * tc.chunks_per_split;
+  const double fixed = 250000.0 + 12.0 * tc.tile_elems;
+  const double split_io = tc.splits > 1 ? (double)tc.bm * tc.bp * (3.0 + tc.splits) * 16.0 : 0.0;
+  const double work = fma + loads + fixed + split_io;
+  const long long ctas = tc.grid * tc.splits * tc.grid_z;
+  const int occ = std::max(1, std::min(max_blocks, tc.occupancy));
+  const double warps = tc.threads / 32.0;
+  auto eff = [&](int k) { return std::min(1.0, k * warps / 12.0); };
+  double t;
+  if (ctas <= (long long)sms * occ) {
+    const int k = (int)cdiv(ctas, sms);
+    t = work * k / eff(k);
+  } else {
+    const double waves = (double)cdiv(ctas, (long long)sms * occ);
+    t = waves * work * occ / eff(occ);
+  }
+  return t + 2.0e6;  // launch + ramp
+}
+
+bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits, bool allow_split,
+              Candidate *out) {
   const Family &f = kFamilies[fam_id];
   const int hf_eff = stage1 ? 1 : g.HF;
   const int wf_eff = stage1 ? 1 : g.WF;
   const int taps = hf_eff * wf_eff;
-  TileChoice tc;
-  tc.family = fam_id;
-  tc.bm = f.bm;
-  tc.bp = f.bp;
-  tc.bc = f.bc;
-  tc.threads = f.threads;
-  tc.rs = (g.Wo - 1) * g.S + wf_eff;
-  tc.rows = max_tile_rows(g, hf_eff, f.bp);
-  const long long tile_elems = (long long)tc.rs * tc.rows;
-  if (tile_elems > (1 << 20)) return false;
-  tc.tile_elems = (int)tile_elems;
-  tc.xcs = (int)((tile_elems + 3) & ~3LL);
-  const int nchunks = (int)cdiv(g.C, f.bc);
-  tc.stages = nchunks > 1 ? 2 : 1;
-  const long long stage_floats = (long long)f.bc * tc.xcs + (long long)f.bc * taps * (f.bm + 4);
-  const long long smem = 4LL * (tc.xcs + tc.stages * stage_floats);
-  if (smem > 227 * 1024) return false;
-  tc.smem_bytes = (int)smem;
+  TileChoice base;
+  base.family = fam_id;
+  base.bm = f.bm;
+  base.bp = f.bp;
+  base.bc = f.bc;
+  base.threads = f.threads;
+  const int rc = (g.Wo - 1) * g.S + wf_eff;
+  base.rs = rc + (((g.W - rc) % 4) + 4) % 4;  // == W (mod 4): rows stay 16B-congruent with global rows
+  base.rows = max_tile_rows(g, hf_eff, f.bp);
+  const long long positions = (long long)base.rs * base.rows + 3;
+  if (positions > (1 << 20)) return false;
+  base.tile_elems = rc * base.rows;
+  base.xcs = (int)((positions + 3) & ~3LL);
   // relative offsets inside a tile must fit int32 (goff table)
   const long long imgs = cdiv(f.bp, g.HoWo) + 2;
   if (imgs * (long long)g.C * g.H * g.W >= INT_MAX) return false;
   const long long mtiles = cdiv(g.M, f.bm);
   const long long ptiles = cdiv(g.Q, f.bp);
-  tc.grid = mtiles * ptiles;
-  tc.grid_z = stage1 ? g.HF * g.WF : 1;
-  const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
-  const int by_threads = 2048 / f.threads;
-  const int occ = std::max(1, std::min({f.max_ctas_per_sm, by_smem, by_threads}));
-  tc.occupancy = occ;
-  const long long total_ctas = tc.grid * tc.grid_z;
-  const double waves = (double)cdiv(total_ctas, (long long)sms * occ);
-  // per-CTA work: FMA lanes plus staging traffic (element loads ~ 8 FMA-lane equivalents)
-  const double fma = (double)f.bm * f.bp * taps * g.C;
-  const double loads = 8.0 * ((double)tile_elems + (double)f.bm * taps) * g.C;
-  const double per_cta = fma * (stage1 ? 2.0 : 1.0) + loads;
-  out->family = fam_id;
-  out->tc = tc;
-  out->cost = waves * occ * per_cta;
+  base.grid = mtiles * ptiles;
+  base.grid_z = stage1 ? g.HF * g.WF : 1;
+  const int nchunks = (int)cdiv(g.C, f.bc);
+
+  Candidate best;
+  const int auto_opts[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
+  const int forced_opts[] = {forced_splits};
+  const int *opts = forced_splits > 0 ? forced_opts : auto_opts;
+  const int nopts = forced_splits > 0 ? 1 : (int)(sizeof(auto_opts) / sizeof(int));
+  for (int oi = 0; oi < nopts; oi++) {
+    const int sp = opts[oi];
+    if (sp > 1 && (stage1 || !allow_split)) break;
+    if (sp > nchunks) {
+      if (forced_splits > 0) return false;
+      break;
+    }
+    TileChoice tc = base;
+    tc.chunks_per_split = (int)cdiv(nchunks, sp);
+    tc.splits = (int)cdiv(nchunks, tc.chunks_per_split);
+    if (tc.splits != sp && forced_splits <= 0) continue;  // duplicate of a smaller split
+    tc.stages = tc.chunks_per_split > 1 ? 2 : 1;
+    const long long stage_floats = (long long)f.bc * tc.xcs + (long long)f.bc * taps * (f.bm + 4);
+    const long long tables = tc.xcs + (((tc.xcs >> 2) + 3) & ~3);
+    const long long smem = 4LL * (tables + tc.stages * stage_floats);
+    if (smem > 226 * 1024) return best.family >= 0 ? (*out = best, true) : false;
+    tc.smem_bytes = (int)smem;
+    const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
+    const int by_threads = 2048 / f.threads;
+    tc.occupancy = std::max(1, std::min({f.max_ctas_per_sm, by_smem, by_threads}));
+    tc.ws_bytes = tc.splits > 1 ? split_counter_bytes(tc.grid) + 4LL * tc.grid * tc.splits * f.bm * f.bp : 0;
+    tc.cost = model_cost(g, tc, taps, stage1, sms, tc.occupancy);
+    if (tc.cost < best.cost) {
+      best.family = fam_id;
+      best.tc = tc;
+      best.cost = tc.cost;
+    }
+  }
+  if (best.family < 0) return false;
+  *out = best;
   return true;
 }
 
@@ -167,31 +217,28 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
 int device_sm_count(int device) { return sm_count_of(device); }
 
 // Planner: returns false if no family can run the geometry.
-bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, TileChoice *out) {
+bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int forced_splits, bool allow_split,
+                TileChoice *out) {
   const int sms = sm_count_of(device);
   Candidate best;
-  bool exact_found = false;
   if (forced_family >= 0) {
     if (!family_matches(forced_family, g, stage1)) return false;
-    if (!evaluate(g, forced_family, stage1, sms, &best)) return false;
+    if (!evaluate(g, forced_family, stage1, sms, forced_splits, allow_split, &best)) return false;
     *out = best.tc;
     return true;
   }
-  for (int pass = 0; pass < 2; pass++) {
+  for (int pass = 0; pass < 2 && best.family < 0; pass++) {
     for (int i = 0; i < kNumFamilies; i++) {
       const Family &f = kFamilies[i];
       if (!family_matches(i, g, stage1)) continue;
       const bool generic = (f.hf == 0) && !stage1;
-      if (pass == 0 && generic) continue;  // prefer specialised families
-      if (pass == 1 && !generic) continue;
+      if ((pass == 0) == generic) continue;  // specialised families first
       Candidate c;
-      if (!evaluate(g, i, stage1, sms, &c)) continue;
-      if (c.cost < best.cost * 0.999 || (c.cost <= best.cost * 1.001 && best.family >= 0 &&
-                                         kFamilies[i].bm > kFamilies[best.family].bm))
+      if (!evaluate(g, i, stage1, sms, forced_splits, allow_split, &c)) continue;
+      if (c.cost < best.cost * 0.999 ||
+          (c.cost <= best.cost * 1.001 && best.family >= 0 && kFamilies[i].bm > kFamilies[best.family].bm))
         best = c;
-      exact_found = true;
     }
-    if (exact_found) break;
   }
   if (best.family < 0) return false;
   *out = best.tc;
@@ -199,14 +246,21 @@ bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, TileC
 }
 
 cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, const float *w, float *y,
-                          bool stage1, long long y_tap_stride, cudaStream_t stream) {
+                          bool stage1, long long y_tap_stride, void *workspace, cudaStream_t stream) {
   const Family &f = kFamilies[tc.family];
   int dev = 0;
   cudaGetDevice(&dev);
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (dev < 64 && !g_attr_done[tc.family][dev]) {
-      cudaError_t e = cudaFuncSetAttribute(f.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncAttributes fa;
+      cudaError_t e = cudaFuncGetAttributes(&fa, f.kernel);
+      if (e != cudaSuccess) return e;
+      int optin = 0;
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      if (optin <= 0) optin = 227 * 1024;
+      e = cudaFuncSetAttribute(f.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               optin - (int)fa.sharedSizeBytes);
       if (e != cudaSuccess) return e;
       g_attr_done[tc.family][dev] = true;
     }
@@ -225,19 +279,44 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   p.Hp = g.Hp;
   p.Q = (int)g.Q;
   p.RS = tc.rs;
+  p.RC = (g.Wo - 1) * g.S + (stage1 ? 1 : g.WF);
   p.ROWS = tc.rows;
   p.XCS = tc.xcs;
-  p.tile_elems = tc.tile_elems;
+  p.vec_ok = ((long long)g.H * g.W % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   p.mtiles = (int)cdiv(g.M, tc.bm);
   p.nchunks = (int)cdiv(g.C, tc.bc);
+  p.splits = tc.splits;
+  p.chunks_per_split = tc.splits > 1 ? tc.chunks_per_split : p.nchunks;
+  if (tc.splits > 1) {
+    if (!workspace) return cudaErrorInvalidValue;
+    p.counters = static_cast<int *>(workspace);
+    p.partials = reinterpret_cast<float *>(static_cast<char *>(workspace) + split_counter_bytes(tc.grid));
+  }
   p.w_ctaps = g.HF * g.WF;
   p.wf_full = g.WF;
   p.y_tap_stride = y_tap_stride;
   p.strict_tap_major = stage1 ? 1 : 0;
+  dim3 grid((unsigned)tc.grid, (unsigned)tc.splits, (unsigned)tc.grid_z);
+  // development tracing: per-CTA SM id and start/end globaltimer to a CSV file
+  const char *trace_file = std::getenv("B2C_TRACE_FILE");
+  const long long nctas = tc.grid * tc.splits * tc.grid_z;
+  unsigned long long *trace = nullptr;
+  if (trace_file && cudaMalloc(&trace, sizeof(unsigned long long) * 3 * nctas) == cudaSuccess) p.trace = trace;
   void *args[] = {&p};
-  dim3 grid((unsigned)tc.grid, 1, (unsigned)tc.grid_z);
   note_launch();
-  return cudaLaunchKernel(f.kernel, grid, dim3(tc.threads), args, (size_t)tc.smem_bytes, stream);
+  cudaError_t err = cudaLaunchKernel(f.kernel, grid, dim3(tc.threads), args, (size_t)tc.smem_bytes, stream);
+  if (trace) {
+    std::vector<unsigned long long> h(3 * nctas);
+    cudaStreamSynchronize(stream);
+    cudaMemcpy(h.data(), trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(trace);
+    if (FILE *fp = std::fopen(trace_file, "a")) {
+      for (long long i = 0; i < nctas; i++)
+        std::fprintf(fp, "%s,%lld,%llu,%llu,%llu\n", f.name, i, h[3 * i], h[3 * i + 1], h[3 * i + 2]);
+      std::fclose(fp);
+    }
+  }
+  return err;
 }
 
 cudaError_t launch_stage2(const float *partials, float *y, long long total, int taps, int device,

@@ -18,17 +18,25 @@ struct TileChoice {
   int rows = 0, rs = 0, xcs = 0, tile_elems = 0;
   int smem_bytes = 0;
   int occupancy = 0;
-  long long grid = 0;
-  int grid_z = 1;
+  long long grid = 0;   // output tiles (m-tiles x pixel tiles)
+  int grid_z = 1;       // stage 1: filter rows
+  int splits = 1;       // fused: channel ranges reduced separately
+  int chunks_per_split = 0;
+  long long ws_bytes = 0;  // workspace needed for splits > 1 (counters + partial tiles)
+  double cost = 0;
 };
+
+// workspace layout for split-C: [counters: tiles ints, padded to 256 B][partials]
+inline long long split_counter_bytes(long long tiles) { return (tiles * 4 + 255) / 256 * 256; }
 
 const char *family_name(int id);
 int num_families();
 bool family_matches(int fam_id, const Geom &g, bool stage1);
 int device_sm_count(int device);
-bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, TileChoice *out);
+bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int forced_splits, bool allow_split,
+                TileChoice *out);
 cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, const float *w, float *y,
-                          bool stage1, long long y_tap_stride, cudaStream_t stream);
+                          bool stage1, long long y_tap_stride, void *workspace, cudaStream_t stream);
 cudaError_t launch_stage2(const float *partials, float *y, long long total, int taps, int device,
                           cudaStream_t stream);
 void note_launch();

@@ -56,7 +56,7 @@ def _check_tensor(t, what: str) -> None:
 class ConvLayer:
     """A resolved forward convolution for one configuration."""
 
-    def __init__(self, cfg: ConvConfig, engine: str = "fused", family: int = -1):
+    def __init__(self, cfg: ConvConfig, engine: str = "fused", family: int = -1, splits: int = 0):
         if engine not in ("fused", "twostage"):
             raise ValueError(f"unknown engine {engine!r}")
         if engine == "twostage" and cfg.stride != 1:
@@ -67,6 +67,7 @@ class ConvLayer:
         self._lib = nat.lib()
         self._tiles = nat.TilePlanC()
         self._tiles.family = int(family)
+        self._tiles.splits = int(splits)
         e = nat.ENGINE_TWOSTAGE if engine == "twostage" else nat.ENGINE_FUSED
         nat.check(self._lib.b2c_select_tiles(ctypes.byref(self._desc), e, ctypes.byref(self._tiles)))
         self.out_hw = output_dims(cfg)
@@ -74,6 +75,8 @@ class ConvLayer:
         if engine == "twostage" and not (cfg.hf == 1 and cfg.wf == 1):
             self.workspace_bytes = int(self._lib.b2c_workspace_bytes(ctypes.byref(self._desc)))
         self._ws = None
+        self.split_workspace_bytes = int(self._tiles.workspace_bytes) if engine == "fused" else 0
+        self._split_ws = None
 
     @property
     def family(self) -> str:
@@ -82,6 +85,10 @@ class ConvLayer:
     @property
     def grid(self) -> int:
         return int(self._tiles.grid)
+
+    @property
+    def splits(self) -> int:
+        return int(self._tiles.splits)
 
     def output_shape(self) -> tuple[int, int, int, int]:
         return (self.cfg.n, self.cfg.m, *self.out_hw)
@@ -93,8 +100,14 @@ class ConvLayer:
             out = torch.empty(self.output_shape(), dtype=torch.float32, device=x.device)
         s = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
         if self.engine == "fused":
+            ws_ptr, ws_len = None, 0
+            if self.split_workspace_bytes:
+                if self._split_ws is None or self._split_ws.device != x.device:
+                    # zero-filled once; every completed launch leaves it zeroed
+                    self._split_ws = torch.zeros(self.split_workspace_bytes, dtype=torch.uint8, device=x.device)
+                ws_ptr, ws_len = self._split_ws.data_ptr(), self.split_workspace_bytes
             st = self._lib.b2c_conv2d_forward(ctypes.byref(self._desc), x.data_ptr(), w.data_ptr(), out.data_ptr(),
-                                              ctypes.byref(self._tiles), ctypes.c_void_p(s))
+                                              ws_ptr, ws_len, ctypes.byref(self._tiles), ctypes.c_void_p(s))
             nat.check(st)
         else:
             if self.workspace_bytes and (self._ws is None or self._ws.device != x.device):

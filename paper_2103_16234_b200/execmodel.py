@@ -78,6 +78,8 @@ class TilePlan:
     smem_row_stride: int
     smem_bytes: int
     grid: int
+    splits: int
+    workspace_bytes: int
 
 
 def _plan_from_c(p: nat.LaunchPlanC) -> LaunchPlan:
@@ -135,12 +137,13 @@ def matching_families(cfg: ConvConfig, engine: str = "fused") -> list[int]:
     return [i for i in range(l.b2c_num_families()) if l.b2c_family_matches(ctypes.byref(d), e, i)]
 
 
-def select_tiles(cfg: ConvConfig, engine: str = "fused", family: int = -1) -> TilePlan:
-    """The B200 tile plan for ``cfg`` (planner's choice, or a forced family)."""
+def select_tiles(cfg: ConvConfig, engine: str = "fused", family: int = -1, splits: int = 0) -> TilePlan:
+    """The B200 tile plan for ``cfg`` (planner's choice, or a forced family / split)."""
     out = nat.TilePlanC()
     out.family = int(family)
+    out.splits = int(splits)
     e = nat.ENGINE_TWOSTAGE if engine == "twostage" else nat.ENGINE_FUSED
     nat.check(nat.lib().b2c_select_tiles(ctypes.byref(nat.desc(cfg)), e, ctypes.byref(out)))
     return TilePlan(nat.lib().b2c_family_name(out.family).decode(), int(out.family), int(out.bm), int(out.bp),
                     int(out.bc), int(out.threads), int(out.stages), int(out.smem_rows), int(out.smem_row_stride),
-                    int(out.smem_bytes), int(out.grid))
+                    int(out.smem_bytes), int(out.grid), int(out.splits), int(out.workspace_bytes))

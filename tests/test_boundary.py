@@ -1,0 +1,272 @@
+"""The drop-in boundary without a GPU: the C ABI library loads and exports
+every symbol include/b2conv.h declares; shape/plan/precondition logic matches
+the reference (golden fixtures + the reference tests' expectations); errors
+surface as the reference's exception classes in the reference's order.  No
+test here launches a kernel."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, cfg_from
+
+import paper_2103_16234_b200 as pk
+from paper_2103_16234_b200 import _native as nat
+
+
+def header_symbols() -> list[str]:
+    text = (ROOT / "include" / "b2conv.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(b2c_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(native):
+    syms = header_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(native, s)]
+    assert not missing, missing
+
+
+def test_binding_covers_header(native):
+    assert set(header_symbols()) == set(nat.SIGNATURES)
+
+
+def test_abi_version(native):
+    assert native.b2c_abi_version() == 1
+
+
+def test_families_enumerable(native):
+    names = pk.family_names()
+    assert len(names) == native.b2c_num_families() >= 10
+    assert any(n.startswith("fused_3x3") for n in names) and any(n.startswith("stage1_strict") for n in names)
+
+
+# --- configs ------------------------------------------------------------------
+
+@pytest.mark.parametrize("field,kwargs", [
+    ("n", dict(n=0)), ("c", dict(c=-1)), ("stride", dict(stride=0)), ("pad_h", dict(pad_h=-1)),
+    ("hf", dict(hf=9, h=3, pad_h=1)), ("wf", dict(wf=6, w=2, pad_w=1)),
+])
+def test_config_validation_names_field(field, kwargs):
+    base = dict(name="t", n=1, c=1, h=5, w=5, m=1, hf=3, wf=3, stride=1, pad_h=0, pad_w=0)
+    base.update(kwargs)
+    with pytest.raises(pk.InvalidConfig) as exc:
+        pk.ConvConfig(**base)
+    assert exc.value.field == field
+
+
+def test_c_abi_config_validation_agrees(native):
+    d = nat.ConvDesc(1, 1, 3, 3, 1, 5, 3, 1, 0, 0)  # hf > h + 2*pad_h
+    bad = ctypes.c_int32(-1)
+    assert native.b2c_validate_config(ctypes.byref(d), ctypes.byref(bad)) == nat.INVALID_CONFIG
+    assert bad.value == 5
+    with pytest.raises(pk.InvalidConfig) as exc:
+        nat.check(native.b2c_validate_config(ctypes.byref(d), None))
+    assert exc.value.field == "hf"
+
+
+def test_output_dims_and_presets():
+    cfg = pk.ConvConfig("t", n=1, c=1, h=224, w=224, m=1, hf=7, wf=7, stride=2, pad_h=3, pad_w=3)
+    assert pk.output_dims(cfg) == (112, 112)
+    names = [c.name for c in pk.preset_configs()]
+    assert names == ["1x1-A", "1x1-B", "1x1-C", "3x3-A", "3x3-B", "5x5-A", "5x5-B"]
+    assert pk.same_padding(5, 5) == (2, 2)
+    with pytest.raises(pk.UnsupportedFilter):
+        pk.same_padding(2, 3)
+
+
+def test_parse_config_file(tmp_path):
+    p = tmp_path / "layers.csv"
+    p.write_text("# comment\nc1, 1, 64, 56, 56, 64, 3, 3, 1, 1, 1\n\nx,2,3,4,5,6,1,1,1,0,0 # tail\n")
+    cfgs = pk.parse_config_file(p)
+    assert [c.name for c in cfgs] == ["c1", "x"] and cfgs[0].pad_w == 1
+    p.write_text("bad,1,2\n")
+    with pytest.raises(pk.ParseError) as exc:
+        pk.parse_config_file(p)
+    assert exc.value.line_no == 1
+    p.write_text("ok,1,1,1,1,1,1,1,1,0,0\nz,1,1,1,1,1,3,1,1,0,0\n")
+    with pytest.raises(pk.InvalidConfig) as exc:
+        pk.parse_config_file(p)
+    assert exc.value.field == "hf"
+
+
+def test_tensor_file_round_trip_preserves_bits(tmp_path):
+    data = np.array([np.nan, -0.0, np.inf, 1e-42, -3.5, 0.0], np.float32).reshape(1, 2, 3, 1)
+    data.view(np.uint32)[0, 0, 0, 0] = 0x7FC01234  # NaN payload
+    t = pk.Tensor4(data)
+    pk.save_tensor(t, tmp_path / "t.c0nv")
+    back = pk.load_tensor(tmp_path / "t.c0nv")
+    assert back.data.tobytes() == data.tobytes()
+    (tmp_path / "bad").write_bytes(b"XXXX" + bytes(18))
+    with pytest.raises(pk.FormatError):
+        pk.load_tensor(tmp_path / "bad")
+
+
+def test_tensor_helpers():
+    t = pk.make_tensor((2, 3, 4, 5), "uniform", seed=7)
+    assert t.data.flags.c_contiguous and t.data.dtype == np.float32
+    assert t.coords(t.flat_index(1, 2, 3, 4)) == (1, 2, 3, 4)
+    assert pk.read_padded(t, 0, 0, -1, 0) == 0.0
+    with pytest.raises(IndexError):
+        pk.read_padded(t, 2, 0, 0, 0)
+    with pytest.raises(pk.InvalidShape):
+        pk.make_tensor((1, 2, 3), "zeros")
+
+
+# --- the launch-plan contract (execmodel.py:36-128) ---------------------------
+
+def test_plan_launch_matches_reference_golden(golden, native):
+    for rec in golden["plans"] + golden["presets"]:
+        dev = pk.DeviceModel(max_threads_per_block=rec.get("max_threads", 1024))
+        p = pk.plan_launch(cfg_from(rec["cfg"]), dev)
+        assert [p.blocks, p.threads_per_block, p.split_per_filter_row, p.dot_products_per_thread] == rec["plan"]
+        pk.validate_plan(p, cfg_from(rec["cfg"]), dev)
+
+
+def test_plan_launch_reference_expectations(native):
+    presets = {c.name: c for c in pk.preset_configs()}
+    a, b = pk.plan_launch(presets["1x1-A"]), pk.plan_launch(presets["1x1-B"])
+    assert (a.blocks, a.threads_per_block, b.blocks, b.threads_per_block) == (256, 64, 1024, 224)  # crit. 4
+    big = pk.plan_launch(pk.ConvConfig("t", n=1, c=1, h=40, w=50, m=1, hf=1, wf=1))
+    assert (big.split_per_filter_row, big.threads_per_block, big.blocks) == (2, 1024, 2)
+    odd = pk.plan_launch(pk.ConvConfig("t", n=1, c=1, h=10, w=10, m=1, hf=1, wf=1), pk.DeviceModel(max_threads_per_block=48))
+    assert odd.threads_per_block == 32
+    with pytest.raises(pk.Unsupported):
+        pk.plan_launch(pk.ConvConfig("t", n=1, c=1, h=5, w=5, m=1, hf=3, wf=3, stride=2))
+
+
+@pytest.mark.parametrize("override", [dict(split_per_filter_row=0), dict(blocks=3), dict(threads_per_block=2048, blocks=2),
+                                      dict(threads_per_block=0, blocks=2), dict(threads_per_block=33),
+                                      dict(dot_products_per_thread=0), dict(threads_per_block=32)])
+def test_validate_plan_rejects(native, override):
+    cfg = pk.ConvConfig("t", n=1, c=1, h=8, w=8, m=2, hf=1, wf=1)
+    good = pk.plan_launch(cfg)
+    fields = dict(blocks=good.blocks, threads_per_block=good.threads_per_block,
+                  split_per_filter_row=good.split_per_filter_row, dot_products_per_thread=good.dot_products_per_thread)
+    fields.update(override)
+    with pytest.raises(pk.InvalidPlan):
+        pk.validate_plan(pk.LaunchPlan(**fields), cfg)
+
+
+def test_device_model_validation():
+    with pytest.raises(pk.InvalidConfig) as exc:
+        pk.DeviceModel(line_bytes=100, element_bytes=8)
+    assert exc.value.field == "line_bytes"
+    assert pk.DeviceModel().elements_per_line == 32
+
+
+def test_block_position_ranges(native):
+    for work, split in [(10, 3), (4096, 4), (7, 7), (1, 1), (1000, 17)]:
+        r = pk.block_position_ranges(work, split)
+        assert r[0][0] == 0 and r[-1][1] == work and len(r) == split
+        assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+        assert max(h - l for l, h in r) - min(h - l for l, h in r) <= 1
+
+
+def test_workspace_bytes(golden, native):
+    for rec in golden["plans"] + golden["presets"]:
+        cfg = cfg_from(rec["cfg"])
+        assert pk.workspace_bytes(cfg) == rec["workspace_bytes"]
+        assert native.b2c_workspace_bytes(ctypes.byref(nat.desc(cfg))) == rec["workspace_bytes"]
+
+
+# --- preconditions, in the reference's order (twostage.py:73-79, 214-224) ------
+
+def _ops(cfg):
+    return pk.make_tensor(pk.input_dims(cfg)), pk.make_tensor(pk.filter_dims(cfg))
+
+
+def test_stride_checked_before_shapes(native):
+    cfg = pk.ConvConfig("t", n=1, c=1, h=5, w=5, m=1, hf=3, wf=3, stride=2)
+    with pytest.raises(pk.Unsupported):
+        pk.conv_twostage(pk.make_tensor((1, 9, 5, 5)), pk.make_tensor((1, 1, 3, 3)), cfg)
+    with pytest.raises(pk.Unsupported):
+        pk.stage1_scalar_prods(*_ops(cfg), cfg)
+
+
+def test_shape_mismatch_before_plan(native):
+    cfg = pk.ConvConfig("t", n=1, c=2, h=4, w=4, m=1, hf=1, wf=1)
+    bad_plan = pk.LaunchPlan(blocks=1, threads_per_block=33, split_per_filter_row=1, dot_products_per_thread=1)
+    with pytest.raises(pk.ShapeMismatch):
+        pk.conv_twostage(pk.make_tensor((1, 3, 4, 4)), pk.make_tensor(pk.filter_dims(cfg)), cfg, plan=bad_plan)
+    with pytest.raises(pk.ShapeMismatch):
+        pk.conv_twostage(pk.make_tensor(pk.input_dims(cfg)), pk.make_tensor((1, 2, 3, 3)), cfg)
+
+
+def test_plan_before_workspace(native):
+    cfg = pk.ConvConfig("t", n=1, c=1, h=4, w=4, m=1, hf=3, wf=3, pad_h=1, pad_w=1)
+    bad_plan = pk.LaunchPlan(blocks=1, threads_per_block=33, split_per_filter_row=1, dot_products_per_thread=1)
+    with pytest.raises(pk.InvalidPlan):
+        pk.conv_twostage(*_ops(cfg), cfg, workspace_limit=0, plan=bad_plan)
+
+
+def test_workspace_exceeded_carries_sizes(native):
+    cfg = next(c for c in pk.preset_configs() if c.name == "5x5-B")
+    with pytest.raises(pk.WorkspaceExceeded) as exc:
+        pk.conv_twostage(*_ops(cfg), cfg, workspace_limit=1000)
+    assert (exc.value.required, exc.value.limit) == (5_017_600, 1000)
+    with pytest.raises(pk.WorkspaceExceeded):
+        pk.stage1_scalar_prods(*_ops(cfg), cfg, workspace_limit=1000)
+
+
+def test_non_tensor_arguments_raise_attribute_error(native):
+    cfg = pk.ConvConfig("t", n=1, c=1, h=3, w=3, m=1, hf=1, wf=1)
+    with pytest.raises(AttributeError):
+        pk.conv_twostage(np.zeros((1, 1, 3, 3), np.float32), pk.make_tensor((1, 1, 1, 1)), cfg)
+
+
+def test_stage2_shape_mismatch(native):
+    cfg = pk.ConvConfig("t", n=1, c=1, h=3, w=3, m=1, hf=3, wf=3, pad_h=1, pad_w=1)
+    with pytest.raises(pk.ShapeMismatch):
+        pk.stage2_sum(pk.PartialSums(np.zeros((8, 1, 1, 3, 3), np.float32)), cfg)
+
+
+def test_c_abi_argument_errors(native):
+    d = nat.desc(pk.ConvConfig("t", n=1, c=1, h=3, w=3, m=1, hf=1, wf=1))
+    st = native.b2c_conv2d_forward(ctypes.byref(d), None, None, None, None, 0, None, None)
+    assert st == nat.INVALID_ARGUMENT
+    assert "null" in nat.last_error()
+    d2 = nat.desc(pk.ConvConfig("t", n=1, c=1, h=3, w=3, m=1, hf=3, wf=3, stride=2))
+    st = native.b2c_conv_twostage(ctypes.byref(d2), None, None, None, None, 0, None, None, 1 << 30, None, None)
+    assert st == nat.UNSUPPORTED
+
+
+# --- the B200 tile planner ----------------------------------------------------
+
+def test_tile_planner_covers_every_baseline_layer(native):
+    from paper_2103_16234_b200 import workloads as W
+
+    for wl, (_, batches) in W.WORKLOADS.items():
+        for n in batches:
+            for cfg in W.layers(wl, n):
+                t = pk.select_tiles(cfg)
+                ho, wo = pk.output_dims(cfg)
+                assert t.smem_bytes <= 227 * 1024
+                tiles = -(-cfg.m // t.bm) * -(-(cfg.n * ho * wo) // t.bp)
+                assert t.grid == tiles * t.splits, (wl, cfg.name)
+                chunks = -(-cfg.c // t.bc)
+                assert 1 <= t.splits <= chunks
+                assert (t.workspace_bytes > 0) == (t.splits > 1)
+                if t.splits > 1:
+                    assert t.workspace_bytes >= 4 * tiles * t.splits * t.bm * t.bp
+                if cfg.stride == 1:
+                    s = pk.select_tiles(cfg, "twostage")
+                    assert s.family.startswith("stage1_strict") and s.splits == 1
+
+
+def test_tile_planner_forced_family_and_split(native):
+    cfg = pk.ConvConfig("t", n=4, c=64, h=14, w=14, m=48, hf=3, wf=3, pad_h=1, pad_w=1)
+    fams = pk.matching_families(cfg)
+    names = pk.family_names()
+    assert any(names[f] == "fused_3x3s1_m32" for f in fams) and any(names[f].startswith("fused_generic") for f in fams)
+    for f in fams:
+        assert pk.select_tiles(cfg, family=f).family_id == f
+    t = pk.select_tiles(cfg, splits=4)
+    assert t.splits == 4
+    with pytest.raises(pk.InvalidPlan):
+        pk.select_tiles(cfg, family=names.index("fused_1x1s1_m32"))
