@@ -165,7 +165,7 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
   const int nopts = forced_splits > 0 ? 1 : (int)(sizeof(auto_opts) / sizeof(int));
   for (int oi = 0; oi < nopts; oi++) {
     const int sp = opts[oi];
-    if (sp > 1 && (stage1 || !allow_split)) break;
+    if (sp > 1 && (stage1 || !allow_split || base.grid > kMaxSplitTiles)) break;
     if (sp > nchunks) {
       if (forced_splits > 0) return false;
       break;

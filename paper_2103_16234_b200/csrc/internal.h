@@ -26,8 +26,12 @@ struct TileChoice {
   double cost = 0;
 };
 
-// workspace layout for split-C: [counters: tiles ints, padded to 256 B][partials]
-inline long long split_counter_bytes(long long tiles) { return (tiles * 4 + 255) / 256 * 256; }
+// workspace layout for split-C: [counters: a fixed region of kMaxSplitTiles ints][partials].
+// The counter region is fixed so that workspaces shared by layers with different
+// plans never see one layer's partials where another keeps its counters (every
+// completed launch leaves its counters at zero; partials never touch the region).
+constexpr long long kMaxSplitTiles = 16384;
+inline long long split_counter_bytes(long long /*tiles*/) { return kMaxSplitTiles * 4; }
 
 const char *family_name(int id);
 int num_families();

@@ -137,15 +137,30 @@ def test_fused_baseline_layers(golden):
         assert oracle.relative_error(got, ref) <= tol(cfg), (cfg.name, cfg.n)
 
 
-def test_fused_special_values_nan_positions(golden, special_arrays):
-    """Non-finite propagation (0*inf over padding, inf-inf) lands on the same
-    outputs as the reference."""
-    for i, c in enumerate(golden["special_values"][:8]):
-        cfg = cfg_from(c)
-        x, w = special_arrays[f"sv{i}_x"], special_arrays[f"sv{i}_w"]
-        want = special_arrays[f"sv{i}_naive"]
+def test_fused_special_values_nan_positions():
+    """Non-finite propagation (0*inf over padding, inf-inf, nan) lands on the
+    same outputs as the reference order.  Finite values are kept far from
+    overflow: near FLT_MAX, whether a partial sum overflows depends on the
+    summation order, which the fused engine does not share (the two-stage
+    engine, which does, is checked bitwise on such cases above)."""
+    import oracle
+
+    rng = np.random.default_rng(77)
+    specials = np.array([np.nan, np.inf, -np.inf, -0.0, 0.0, 1e-40], np.float32)
+    for i in range(12):
+        f = int(rng.choice((1, 3, 5)))
+        p = int(rng.integers(0, f))
+        cfg = pk.ConvConfig(f"fs{i}", n=int(rng.integers(1, 3)), c=int(rng.integers(1, 20)),
+                            h=int(rng.integers(f, 12)), w=int(rng.integers(f, 12)), m=int(rng.integers(1, 40)),
+                            hf=f, wf=f, pad_h=p, pad_w=p)
+        x = rng.uniform(-2, 2, pk.input_dims(cfg)).astype(np.float32)
+        w = rng.uniform(-2, 2, pk.filter_dims(cfg)).astype(np.float32)
+        kx, kw = rng.random(x.shape) < 0.03, rng.random(w.shape) < 0.03
+        x[kx] = rng.choice(specials, int(kx.sum()))
+        w[kw] = rng.choice(specials, int(kw.sum()))
+        want = oracle.conv_naive(cfg, x, w)
         got = pk.conv_forward(pk.Tensor4(x), pk.Tensor4(w), cfg).data
-        assert np.array_equal(np.isnan(got), np.isnan(want)), cfg.name
+        assert np.array_equal(np.isnan(got), np.isnan(want)), cfg
         inf = np.isinf(want)
         assert np.array_equal(np.isinf(got), inf) and np.array_equal(np.sign(got[inf]), np.sign(want[inf]))
 
