@@ -134,18 +134,23 @@ b2c_status b2c_block_position_ranges(int64_t work, int64_t split, int64_t *lo_hi
  * entry that family is forced (B2C_INVALID_PLAN if it cannot run d). */
 b2c_status b2c_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tile_plan *out);
 
+/* Register a measured plan (tools/autotune.py "find" result) for an exact
+ * shape: the planner then uses (family, splits) for it instead of its cost
+ * model.  The Python package registers paper_2103_16234_b200/tuned_plans.json
+ * at import. */
+b2c_status b2c_register_tuned_plan(const b2c_conv_desc *d, int32_t engine, int32_t family, int32_t splits);
+
 /* ------------------------------------------------- device-pointer compute */
 /* Fused direct convolution (any stride >= 1, any padding).  Replaces the
  * compute of twostage.conv_twostage (twostage.py:208-239) and
  * reference.conv_naive (reference.py:58-83) for device-resident tensors.
  * `tiles` may be NULL (planner's choice) or carry a forced family / split.
  * Layers with too few output tiles for 148 SMs are split over channel ranges
- * (split-C) whose partials the tile's last CTA combines in ascending order;
- * that needs `workspace` (tiles.workspace_bytes from b2c_select_tiles), which
- * must be zero-filled before its first use and is left zeroed by every
- * completed launch.  With no (or too small a) workspace the planner picks an
- * unsplit plan.  Per output, the summation order is a function of
- * (c, hf, wf, splits) only. */
+ * (split-C): each range writes a partial plane into `workspace`
+ * (tiles.workspace_bytes from b2c_select_tiles, splits*N*M*Ho*Wo*4 bytes) and
+ * a second launch adds the planes in ascending range order.  With no (or too
+ * small a) workspace the planner picks an unsplit plan.  Per output, the
+ * summation order is a function of (c, hf, wf, splits) only. */
 b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
                               int64_t workspace_size, const b2c_tile_plan *tiles, void *stream);
 

@@ -68,6 +68,7 @@ SIGNATURES = {
     "b2c_validate_plan": (ctypes.c_int, [_P(ConvDesc), _P(DeviceModelC), _P(LaunchPlanC)]),
     "b2c_block_position_ranges": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, _P(ctypes.c_int64)]),
     "b2c_select_tiles": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, _P(TilePlanC)]),
+    "b2c_register_tuned_plan": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     "b2c_conv2d_forward": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, ctypes.c_void_p, ctypes.c_int64,
                                           _P(TilePlanC), ctypes.c_void_p]),
     "b2c_conv_twostage": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _fp, ctypes.c_int64, _P(LaunchPlanC),
@@ -109,7 +110,30 @@ def lib():
                 fn.restype = res
                 fn.argtypes = args
             _lib = l
+            _register_tuned(l)
     return _lib
+
+
+TUNED_PATH = Path(__file__).resolve().parent / "tuned_plans.json"
+
+
+def _register_tuned(l) -> None:
+    """Register the measured plans shipped with the package (if any)."""
+    import json
+
+    if not TUNED_PATH.exists():
+        return
+    try:
+        entries = json.loads(TUNED_PATH.read_text()).get("plans", [])
+    except (OSError, ValueError):
+        return
+    names = [l.b2c_family_name(i).decode() for i in range(l.b2c_num_families())]
+    for e in entries:
+        if e.get("family") not in names:
+            continue
+        d = ConvDesc(*[int(v) for v in e["desc"]])
+        eng = ENGINE_TWOSTAGE if e.get("engine") == "twostage" else ENGINE_FUSED
+        l.b2c_register_tuned_plan(ctypes.byref(d), eng, names.index(e["family"]), int(e.get("splits", 1)))
 
 
 def last_error() -> str:

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdint>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -111,9 +112,10 @@ struct PlanKey {
   int forced;
   int forced_splits;
   int allow_split;
+  int allow_vec;
   bool operator==(const PlanKey &o) const {
     return std::memcmp(&d, &o.d, sizeof(d)) == 0 && stage1 == o.stage1 && device == o.device && forced == o.forced &&
-           forced_splits == o.forced_splits && allow_split == o.allow_split;
+           forced_splits == o.forced_splits && allow_split == o.allow_split && allow_vec == o.allow_vec;
   }
 };
 struct PlanKeyHash {
@@ -128,7 +130,7 @@ std::mutex g_plan_mu;
 std::unordered_map<PlanKey, b2c::TileChoice, PlanKeyHash> g_plans;
 
 b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, int forced, int forced_splits,
-                     bool allow_split, b2c::TileChoice *tc) {
+                     bool allow_split, b2c::TileChoice *tc, bool allow_vec = true) {
   int device = 0;
   cudaGetDevice(&device);
   PlanKey key;
@@ -139,6 +141,7 @@ b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, in
   key.forced = forced;
   key.forced_splits = forced_splits;
   key.allow_split = allow_split;
+  key.allow_vec = allow_vec;
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_plans.find(key);
@@ -147,7 +150,7 @@ b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, in
       return B2C_OK;
     }
   }
-  if (!b2c::plan_tiles(g, stage1, device, forced, forced_splits, allow_split, tc)) {
+  if (!b2c::plan_tiles(g, stage1, device, forced, forced_splits, allow_split, allow_vec, tc)) {
     if (forced >= 0 || forced_splits > 0)
       return fail(B2C_INVALID_PLAN, "tile family %d (%s) / split %d cannot run this configuration", forced,
                   forced >= 0 ? b2c::family_name(forced) : "auto", forced_splits);
@@ -222,7 +225,7 @@ b2c_status run_stage1(const b2c_conv_desc *d, const b2c::Geom &g, const float *x
 }
 
 // ------------------------------------------------------ host staging cache
-// slots: 0 x, 1 w, 2 y, 3 two-stage partial planes, 4 split-C workspace (kept zeroed)
+// slots: 0 x, 1 w, 2 y, 3 two-stage partial planes, 4 split-C partial planes
 struct DeviceBuffers {
   void *ptr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   size_t cap[5] = {0, 0, 0, 0, 0};
@@ -238,8 +241,6 @@ b2c_status ensure(DeviceBuffers &b, int slot, size_t bytes) {
   b.cap[slot] = 0;
   cudaError_t e = cudaMalloc(&b.ptr[slot], bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-  e = cudaMemset(b.ptr[slot], 0, bytes);  // split-C counters (slot 4) must start at zero
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMemset");
   b.cap[slot] = bytes;
   return B2C_OK;
 }
@@ -379,6 +380,19 @@ b2c_status b2c_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tile_pla
   return B2C_OK;
 }
 
+b2c_status b2c_register_tuned_plan(const b2c_conv_desc *d, int32_t engine, int32_t family, int32_t splits) {
+  b2c_status st = check_config(d, nullptr);
+  if (st != B2C_OK) return st;
+  b2c::Geom g = geom_of(d);
+  const bool stage1 = engine == B2C_ENGINE_TWOSTAGE;
+  if (!b2c::family_matches(family, g, stage1))
+    return fail(B2C_INVALID_PLAN, "family %d cannot run this configuration", family);
+  b2c::register_tuned(g, stage1, family, splits);
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  g_plans.clear();  // cached plans may predate the registration
+  return B2C_OK;
+}
+
 int32_t b2c_family_matches(const b2c_conv_desc *d, int32_t engine, int32_t family) {
   if (check_config(d, nullptr) != B2C_OK) return 0;
   return b2c::family_matches(family, geom_of(d), engine == B2C_ENGINE_TWOSTAGE) ? 1 : 0;
@@ -396,11 +410,16 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
   b2c::TileChoice tc;
   st = get_tiles(d, g, false, forced, forced_splits, true, &tc);
   if (st != B2C_OK) return st;
-  if (tc.splits > 1 && (!workspace || workspace_size < tc.ws_bytes)) {
-    if (forced_splits > 1)
-      return fail(B2C_INVALID_ARGUMENT, "split %d needs a %lld-byte workspace, %lld provided", forced_splits,
-                  (long long)tc.ws_bytes, (long long)workspace_size);
-    st = get_tiles(d, g, false, forced, 0, false, &tc);  // unsplit plan
+  const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                         reinterpret_cast<uintptr_t>(workspace)) & 15) == 0;
+  const bool ws_ok = tc.splits <= 1 || (workspace && workspace_size >= tc.ws_bytes);
+  if (!ws_ok && forced_splits > 1)
+    return fail(B2C_INVALID_ARGUMENT, "split %d needs a %lld-byte workspace, %lld provided", forced_splits,
+                (long long)tc.ws_bytes, (long long)workspace_size);
+  if (tc.kind == 1 && !aligned && forced >= 0)
+    return fail(B2C_INVALID_ARGUMENT, "family %s needs 16-byte aligned x, y and workspace", b2c::family_name(forced));
+  if (!ws_ok || (tc.kind == 1 && !aligned)) {
+    st = get_tiles(d, g, false, forced, ws_ok ? forced_splits : 0, ws_ok, &tc, aligned);
     if (st != B2C_OK) return st;
   }
   cudaError_t e = b2c::launch_direct(g, tc, x, w, y, false, 0, workspace, (cudaStream_t)stream);

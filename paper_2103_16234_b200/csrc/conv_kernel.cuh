@@ -45,8 +45,8 @@ struct KParams {
   const float *x;
   const float *w;
   float *y;
-  float *partials;   // split-C partial tiles: [tile][split][BM*BP]
-  int *counters;     // split-C arrival counters, one per tile, zero between launches
+  float *partials;   // split-C partial planes: [split][n][m][ho][wo]
+  long long part_stride;  // elements per partial plane (N*M*Ho*Wo)
   int N, C, H, W, M;
   int S;             // stride
   int HF, WF;        // filter extent handled by THIS launch (1x1 for stage 1)
@@ -67,13 +67,19 @@ struct KParams {
   int wf_full;       // wf of the full filter (stage 1 decodes k -> (yf, xf))
   long long y_tap_stride;  // stage 1: elements between partial planes of consecutive k
   int strict_tap_major;    // stage 1: blockIdx.z selects the filter row
-  unsigned long long *trace;  // optional per-CTA (smid, t_start, t_end) records (B2C_TRACE_FILE)
+  unsigned long long *trace;  // optional per-CTA (smid, t_start, t_tables, t_loop, t_end) records
+  unsigned long long mRS, mHp, mHoWo, mWo;  // exact division magics: floor(2^32/d) + 1
+  int pdl;                    // launched with programmatic dependent launch
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+// floor(x / d) for 0 <= x < 2^20 via a host-computed magic m = floor(2^32/d) + 1
+__device__ __forceinline__ int fdiv(int x, unsigned long long m) {
+  return (int)(((unsigned long long)(unsigned)x * m) >> 32);
 }
 __device__ __forceinline__ unsigned smid() {
   unsigned s;
@@ -129,7 +135,6 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
   const int xfloats = BC * p.XCS;
   const int stage_floats = xfloats + BC * taps * WS;
   float *stage0 = smem + p.XCS + ((ngroups + 3) & ~3);
-  __shared__ int s_last;
 
   const int tid = threadIdx.x;
   const unsigned long long t_start = p.trace ? global_ns() : 0ull;
@@ -152,8 +157,8 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
   }
 
   // ---- tile origin in virtual-row space -----------------------------------
-  const int n0 = q0 / p.HoWo;
-  const int oy0 = (q0 - n0 * p.HoWo) / p.Wo;
+  const int n0 = q0 / p.HoWo;  // q0 may exceed 2^20: exact hardware division once per CTA
+  const int oy0 = fdiv(q0 - n0 * p.HoWo, p.mWo);
   const int vlo = n0 * p.Hp + oy0 * S + tap_y;
   const long long chw = (long long)p.C * p.H * p.W;
   const int hw = p.H * p.W;
@@ -167,15 +172,16 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
     const int rel = pos - shift;
     int g = -2;
     if (rel >= 0) {
-      const int r = rel / p.RS;
+      const int r = fdiv(rel, p.mRS);
       const int col = rel - r * p.RS;
       if (r < p.ROWS && col < p.RC) {
-        const int v = vlo + r;
-        const int n = v / p.Hp;
-        const int iy = v - n * p.Hp - p.PH;
+        const int vrel = vlo - n0 * p.Hp + r;  // virtual row relative to image n0 (< 2^20)
+        const int dn = fdiv(vrel, p.mHp);
+        const int n = n0 + dn;
+        const int iy = vrel - dn * p.Hp - p.PH;
         const int ix = col + tap_x - p.PW;
         const bool ok = (n < p.N) && (iy >= 0) && (iy < p.H) && (ix >= 0) && (ix < p.W);
-        g = ok ? (int)((long long)(n - n0) * chw + iy * p.W + ix) : -1;
+        g = ok ? (int)((long long)dn * chw + iy * p.W + ix) : -1;
       }
     }
     goff[pos] = g;
@@ -192,17 +198,23 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
   }
 
   // ---- per-thread output pixels: shared-memory offsets of their windows ----
+  const long long trace_cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   int pix_off[RP];
 #pragma unroll
   for (int j = 0; j < RP; j++) {
-    const int q = min(q0 + j * NTP + tp, p.Q - 1);
-    const int n = q / p.HoWo;
-    const int rem = q - n * p.HoWo;
-    const int oy = rem / p.Wo;
+    const int qr = min(q0 + j * NTP + tp, p.Q - 1) - n0 * p.HoWo;  // relative to image n0 (< 2^20)
+    const int dn = fdiv(qr, p.mHoWo);
+    const int rem = qr - dn * p.HoWo;
+    const int oy = fdiv(rem, p.mWo);
     const int ox = rem - oy * p.Wo;
-    pix_off[j] = shift + ((n - n0) * p.Hp + (oy - oy0) * S) * p.RS + ox * S;
+    pix_off[j] = shift + (dn * p.Hp + (oy - oy0) * S) * p.RS + ox * S;
   }
   __syncthreads();  // tables visible
+  if (p.trace && tid == 0) {
+    p.trace[5 * trace_cta] = smid();
+    p.trace[5 * trace_cta + 1] = t_start;
+    p.trace[5 * trace_cta + 2] = global_ns();
+  }
 
   const float *xtile = p.x + (long long)n0 * chw;
   const bool w_dense = (p.w_ctaps == taps);  // fused: filter taps of a channel are contiguous
@@ -273,6 +285,9 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
   }
 
   // ---- main loop: double-buffered channel chunks of this split --------------
+  // Programmatic dependent launch: everything above (tables, addressing) overlaps
+  // the previous kernel's tail; inputs are read only after it has completed.
+  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   const int chunk_begin = split * p.chunks_per_split;
   const int chunk_end = min(p.nchunks, chunk_begin + p.chunks_per_split);
   if (chunk_begin < chunk_end) {
@@ -345,12 +360,11 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
     return (i & 1) ? acc2[i >> 1][j].y : acc2[i >> 1][j].x;
   };
 
-  if (p.trace && tid == 0) {
-    const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    p.trace[3 * cta] = smid();
-    p.trace[3 * cta + 1] = t_start;
-    p.trace[3 * cta + 2] = global_ns();
-  }
+  if (p.trace && tid == 0) p.trace[5 * trace_cta + 3] = global_ns();
+  if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  auto trace_end = [&]() {
+    if (p.trace && tid == 0) p.trace[5 * trace_cta + 4] = global_ns();
+  };
   // ---- epilogue ---------------------------------------------------------------
   float *yout = p.y;
   if (p.strict_tap_major) yout += (long long)blockIdx.z * p.y_tap_stride;
@@ -366,71 +380,26 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
   }
   const long long plane = p.HoWo;
 
-  if (p.splits == 1) {
-    // fully overwrite y
-#pragma unroll
-    for (int i = 0; i < RM; i++) {
-      const int m = m0 + mg * RM + i;
-      if (m >= p.M) break;
-#pragma unroll
-      for (int j = 0; j < RP; j++)
-        if (pix_ok[j]) yout[out_off[j] + (long long)m * plane] = acc_at(i, j);
-    }
-    return;
-  }
-
-  // split-C: publish this range's partial tile, the last CTA of the tile
-  // combines the ranges in ascending order and writes y.
-  constexpr int TILE = BM * BP;
-  float *mine = p.partials + ((long long)tile * p.splits + split) * TILE;
-#pragma unroll
-  for (int i = 0; i < RM; i++)
-#pragma unroll
-    for (int j = 0; j < RP; j++) mine[(mg * RM + i) * BP + j * NTP + tp] = acc_at(i, j);
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const int prev = atomicAdd(&p.counters[tile], 1);
-    s_last = (prev == p.splits - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  // combine in ascending split order; all RM*RP loads of one split are in
-  // flight together (the order of the adds per output is unchanged)
-  const float *base = p.partials + (long long)tile * p.splits * TILE + mg * RM * BP + tp;
-  float sum[RM][RP];
-#pragma unroll
-  for (int i = 0; i < RM; i++)
-#pragma unroll
-    for (int j = 0; j < RP; j++) sum[i][j] = __ldcg(base + i * BP + j * NTP);
-  for (int s = 1; s < p.splits; s++) {
-    const float *ps = base + (long long)s * TILE;
-    float v[RM][RP];
-#pragma unroll
-    for (int i = 0; i < RM; i++)
-#pragma unroll
-      for (int j = 0; j < RP; j++) v[i][j] = __ldcg(ps + i * BP + j * NTP);
-#pragma unroll
-    for (int i = 0; i < RM; i++)
-#pragma unroll
-      for (int j = 0; j < RP; j++) sum[i][j] = __fadd_rn(sum[i][j], v[i][j]);
-  }
+  // splits == 1: fully overwrite y.  splits > 1: this channel range's partial
+  // goes to plane `split` of the workspace (y layout); stage2_sum_kernel then
+  // adds the planes in ascending order (deterministic, no atomics).
+  float *dst = p.splits > 1 ? p.partials + (long long)split * p.part_stride : yout;
 #pragma unroll
   for (int i = 0; i < RM; i++) {
     const int m = m0 + mg * RM + i;
     if (m >= p.M) break;
 #pragma unroll
     for (int j = 0; j < RP; j++)
-      if (pix_ok[j]) yout[out_off[j] + (long long)m * plane] = sum[i][j];
+      if (pix_ok[j]) dst[out_off[j] + (long long)m * plane] = acc_at(i, j);
   }
-  if (tid == 0) p.counters[tile] = 0;  // leave the workspace zeroed for the next launch
+  trace_end();
 }
 
 // Stage 2 (twostage.py:175-205): y = +0.0 + p_0 + p_1 + ... + p_{k-1}, every
 // add rounded (FADD, never contracted).  HBM-bound streaming kernel.
 __global__ void __launch_bounds__(256) stage2_sum_kernel(const float *__restrict__ partials, float *__restrict__ y,
-                                                         long long total, int taps) {
+                                                         long long total, int taps, int pdl) {
+  if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // partials come from the previous grid
   const long long stride = (long long)gridDim.x * blockDim.x;
   if ((total & 3) == 0) {
     const long long total4 = total >> 2;

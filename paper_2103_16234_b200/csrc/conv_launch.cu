@@ -19,6 +19,7 @@
 #include <vector>
 #include <cstdio>
 
+#include "conv1x1_vec.cuh"
 #include "conv_kernel.cuh"
 #include "internal.h"
 
@@ -34,17 +35,27 @@ struct Family {
   int threads;
   const void *kernel;
   int max_ctas_per_sm;  // from __launch_bounds__
+  int kind;             // 0: conv_direct_kernel (halo staging), 1: conv1x1_vec_kernel
+  int stages;           // cp.async pipeline depth of kind 1
 };
 
 #define B2C_FAMILY(NAME, HF, WF, S, BM, BP, BC, STRICT)                                                    \
   Family {                                                                                                 \
     NAME, HF, WF, S, BM, BP, BC, STRICT, ConvTile<HF, WF, S, BM, BP, BC, STRICT>::NT,                     \
         reinterpret_cast<const void *>(&conv_direct_kernel<HF, WF, S, BM, BP, BC, STRICT>),                \
-        ConvTile<HF, WF, S, BM, BP, BC, STRICT>::MIN_BLOCKS                                                \
+        ConvTile<HF, WF, S, BM, BP, BC, STRICT>::MIN_BLOCKS, 0, 2                                          \
+  }
+
+#define B2C_VEC1X1(NAME, WM, WP, BC)                                                                       \
+  Family {                                                                                                 \
+    NAME, 1, 1, 1, Vec1x1Tile<WM, WP, BC>::BM, Vec1x1Tile<WM, WP, BC>::BP, BC, false,                      \
+        Vec1x1Tile<WM, WP, BC>::NT, reinterpret_cast<const void *>(&conv1x1_vec_kernel<WM, WP, BC>),       \
+        Vec1x1Tile<WM, WP, BC>::MIN_BLOCKS, 1, Vec1x1Tile<WM, WP, BC>::STAGES                              \
   }
 
 const Family kFamilies[] = {
     // fused FFMA2 families
+    B2C_FAMILY("fused_1x1s1_m16", 1, 1, 1, 16, 512, 16, false),
     B2C_FAMILY("fused_1x1s1_m32", 1, 1, 1, 32, 256, 16, false),
     B2C_FAMILY("fused_1x1s1_m64", 1, 1, 1, 64, 256, 16, false),
     B2C_FAMILY("fused_1x1s1_m128", 1, 1, 1, 128, 256, 16, false),
@@ -61,6 +72,11 @@ const Family kFamilies[] = {
     B2C_FAMILY("fused_7x7s2_m64", 7, 7, 2, 64, 256, 4, false),
     B2C_FAMILY("fused_generic_m64", 0, 0, 0, 64, 256, 4, false),
     B2C_FAMILY("fused_generic_m32", 0, 0, 0, 32, 256, 4, false),
+    // pointwise 16-byte families (1x1, stride 1, no padding, H*W % 4 == 0)
+    B2C_VEC1X1("fused_1x1v_m32", 1, 4, 16),
+    B2C_VEC1X1("fused_1x1v_m64", 2, 4, 16),
+    B2C_VEC1X1("fused_1x1v_m64p128", 2, 2, 16),
+    B2C_VEC1X1("fused_1x1v_m128", 4, 2, 16),
     // paper-faithful stage 1 (strict FMUL+FADD, one filter row per blockIdx.z)
     B2C_FAMILY("stage1_strict_m32", 1, 1, 1, 32, 256, 16, true),
     B2C_FAMILY("stage1_strict_m64", 1, 1, 1, 64, 256, 16, true),
@@ -113,7 +129,7 @@ double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, in
   const double per_elem = ((long long)g.H * g.W % 4 == 0) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
   const double loads = (per_elem * tc.tile_elems + 4.0 * tc.bm * taps) * tc.bc * tc.chunks_per_split;
   const double fixed = 250000.0 + 12.0 * tc.tile_elems;
-  const double split_io = tc.splits > 1 ? (double)tc.bm * tc.bp * (3.0 + tc.splits) * 16.0 : 0.0;
+  const double split_io = tc.splits > 1 ? (double)tc.bm * tc.bp * 24.0 : 0.0;  // partial store per CTA
   const double work = fma + loads + fixed + split_io;
   const long long ctas = tc.grid * tc.splits * tc.grid_z;
   const int occ = std::max(1, std::min(max_blocks, tc.occupancy));
@@ -127,7 +143,10 @@ double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, in
     const double waves = (double)cdiv(ctas, (long long)sms * occ);
     t = waves * work * occ / eff(occ);
   }
-  return t + 2.0e6;  // launch + ramp
+  double reduce = 0.0;  // stage-2 style sum of the split planes: launch + 2*(splits+1) plane passes
+  if (tc.splits > 1)
+    reduce = 1.5e6 + 2.0 * (tc.splits + 1) * (double)g.N * g.M * g.HoWo * 4.0 * 168.0 / 40.0 / sms;
+  return t + reduce + 2.0e6;  // launch + ramp
 }
 
 bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits, bool allow_split,
@@ -142,6 +161,50 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
   base.bp = f.bp;
   base.bc = f.bc;
   base.threads = f.threads;
+  base.kind = f.kind;
+  if (f.kind == 1) {
+    base.rs = g.W;
+    base.rows = 1;
+    base.tile_elems = f.bp;
+    base.xcs = f.bp;
+    const long long mtiles = cdiv(g.M, f.bm);
+    base.grid = mtiles * cdiv(g.Q, f.bp);
+    base.grid_z = 1;
+    const int nchunks = (int)cdiv(g.C, f.bc);
+    Candidate best;
+    const int auto_opts[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
+    const int forced_opts[] = {forced_splits};
+    const int *opts = forced_splits > 0 ? forced_opts : auto_opts;
+    const int nopts = forced_splits > 0 ? 1 : (int)(sizeof(auto_opts) / sizeof(int));
+    for (int oi = 0; oi < nopts; oi++) {
+      const int sp = opts[oi];
+      if (sp > 1 && !allow_split) break;
+      if (sp > nchunks) {
+        if (forced_splits > 0) return false;
+        break;
+      }
+      TileChoice tc = base;
+      tc.chunks_per_split = (int)cdiv(nchunks, sp);
+      tc.splits = (int)cdiv(nchunks, tc.chunks_per_split);
+      if (tc.splits != sp && forced_splits <= 0) continue;
+      tc.stages = f.stages;
+      const long long smem = 4LL * f.stages * ((long long)f.bc * f.bp + (long long)f.bc * (f.bm + 4));
+      if (smem > 226 * 1024) return false;
+      tc.smem_bytes = (int)smem;
+      const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
+      tc.occupancy = std::max(1, std::min({f.max_ctas_per_sm, by_smem, 2048 / f.threads}));
+      tc.ws_bytes = tc.splits > 1 ? 4LL * tc.splits * g.N * g.M * g.HoWo : 0;
+      tc.cost = model_cost(g, tc, 1, false, sms, tc.occupancy);
+      if (tc.cost < best.cost) {
+        best.family = fam_id;
+        best.tc = tc;
+        best.cost = tc.cost;
+      }
+    }
+    if (best.family < 0) return false;
+    *out = best;
+    return true;
+  }
   const int rc = (g.Wo - 1) * g.S + wf_eff;
   base.rs = rc + (((g.W - rc) % 4) + 4) % 4;  // == W (mod 4): rows stay 16B-congruent with global rows
   base.rows = max_tile_rows(g, hf_eff, f.bp);
@@ -165,7 +228,7 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
   const int nopts = forced_splits > 0 ? 1 : (int)(sizeof(auto_opts) / sizeof(int));
   for (int oi = 0; oi < nopts; oi++) {
     const int sp = opts[oi];
-    if (sp > 1 && (stage1 || !allow_split || base.grid > kMaxSplitTiles)) break;
+    if (sp > 1 && (stage1 || !allow_split)) break;
     if (sp > nchunks) {
       if (forced_splits > 0) return false;
       break;
@@ -183,7 +246,7 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
     const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
     const int by_threads = 2048 / f.threads;
     tc.occupancy = std::max(1, std::min({f.max_ctas_per_sm, by_smem, by_threads}));
-    tc.ws_bytes = tc.splits > 1 ? split_counter_bytes(tc.grid) + 4LL * tc.grid * tc.splits * f.bm * f.bp : 0;
+    tc.ws_bytes = tc.splits > 1 ? 4LL * tc.splits * g.N * g.M * g.HoWo : 0;
     tc.cost = model_cost(g, tc, taps, stage1, sms, tc.occupancy);
     if (tc.cost < best.cost) {
       best.family = fam_id;
@@ -198,6 +261,11 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
 
 }  // namespace
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("B2C_NO_PDL") == nullptr;
+  return on;
+}
+
 const char *family_name(int id) {
   if (id < 0 || id >= kNumFamilies) return "invalid";
   return kFamilies[id].name;
@@ -209,6 +277,8 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
   if (fam_id < 0 || fam_id >= kNumFamilies) return false;
   const Family &f = kFamilies[fam_id];
   if (f.strict != stage1) return false;
+  if (f.kind == 1)
+    return g.HF == 1 && g.WF == 1 && g.S == 1 && g.PH == 0 && g.PW == 0 && ((long long)g.H * g.W) % 4 == 0;
   if (stage1) return g.S == 1;
   if (f.hf == 0) return true;  // generic
   return f.hf == g.HF && f.wf == g.WF && f.s == g.S;
@@ -216,11 +286,50 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
 
 int device_sm_count(int device) { return sm_count_of(device); }
 
+// Measured plans ("find" results of tools/autotune.py, registered at import by
+// the Python package): exact (shape, engine) -> (family, splits).
+struct TunedKey {
+  int v[11];
+  bool operator==(const TunedKey &o) const { return std::memcmp(v, o.v, sizeof(v)) == 0; }
+};
+struct TunedHash {
+  size_t operator()(const TunedKey &k) const {
+    size_t h = 1469598103934665603ULL;
+    for (int x : k.v) h = (h ^ (size_t)(unsigned)x) * 1099511628211ULL;
+    return h;
+  }
+};
+std::unordered_map<TunedKey, std::pair<int, int>, TunedHash> g_tuned;
+std::mutex g_tuned_mu;
+
+TunedKey tuned_key(const Geom &g, bool stage1) {
+  return TunedKey{{g.N, g.C, g.H, g.W, g.M, g.HF, g.WF, g.S, g.PH, g.PW, stage1 ? 1 : 0}};
+}
+
+void register_tuned(const Geom &g, bool stage1, int family, int splits) {
+  std::lock_guard<std::mutex> lk(g_tuned_mu);
+  g_tuned[tuned_key(g, stage1)] = {family, splits};
+}
+
 // Planner: returns false if no family can run the geometry.
 bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int forced_splits, bool allow_split,
-                TileChoice *out) {
+                bool allow_vec, TileChoice *out) {
   const int sms = sm_count_of(device);
   Candidate best;
+  if (forced_family < 0 && forced_splits <= 0) {
+    std::pair<int, int> t{-1, 0};
+    {
+      std::lock_guard<std::mutex> lk(g_tuned_mu);
+      auto it = g_tuned.find(tuned_key(g, stage1));
+      if (it != g_tuned.end()) t = it->second;
+    }
+    if (t.first >= 0 && (allow_split || t.second <= 1) && (allow_vec || kFamilies[t.first].kind == 0) &&
+        family_matches(t.first, g, stage1) &&
+        evaluate(g, t.first, stage1, sms, t.second, allow_split, &best)) {
+      *out = best.tc;
+      return true;
+    }
+  }
   if (forced_family >= 0) {
     if (!family_matches(forced_family, g, stage1)) return false;
     if (!evaluate(g, forced_family, stage1, sms, forced_splits, allow_split, &best)) return false;
@@ -231,6 +340,7 @@ bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int f
     for (int i = 0; i < kNumFamilies; i++) {
       const Family &f = kFamilies[i];
       if (!family_matches(i, g, stage1)) continue;
+      if (!allow_vec && f.kind == 1) continue;
       const bool generic = (f.hf == 0) && !stage1;
       if ((pass == 0) == generic) continue;  // specialised families first
       Candidate c;
@@ -262,6 +372,10 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
       e = cudaFuncSetAttribute(f.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                optin - (int)fa.sharedSizeBytes);
       if (e != cudaSuccess) return e;
+      // full shared-memory carveout: the planner's occupancy assumes 228 KB per SM
+      e = cudaFuncSetAttribute(f.kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               (int)cudaSharedmemCarveoutMaxShared);
+      if (e != cudaSuccess) return e;
       g_attr_done[tc.family][dev] = true;
     }
   }
@@ -289,30 +403,56 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   p.chunks_per_split = tc.splits > 1 ? tc.chunks_per_split : p.nchunks;
   if (tc.splits > 1) {
     if (!workspace) return cudaErrorInvalidValue;
-    p.counters = static_cast<int *>(workspace);
-    p.partials = reinterpret_cast<float *>(static_cast<char *>(workspace) + split_counter_bytes(tc.grid));
+    p.partials = static_cast<float *>(workspace);
+    p.part_stride = (long long)g.N * g.M * g.HoWo;
   }
   p.w_ctaps = g.HF * g.WF;
   p.wf_full = g.WF;
   p.y_tap_stride = y_tap_stride;
   p.strict_tap_major = stage1 ? 1 : 0;
+  auto magic = [](int d) { return (unsigned long long)((1ULL << 32) / (unsigned long long)d) + 1ULL; };
+  p.mRS = magic(tc.rs);
+  p.mHp = magic(g.Hp);
+  p.mHoWo = magic(g.HoWo);
+  p.mWo = magic(g.Wo);
+  p.pdl = pdl_enabled() ? 1 : 0;
   dim3 grid((unsigned)tc.grid, (unsigned)tc.splits, (unsigned)tc.grid_z);
   // development tracing: per-CTA SM id and start/end globaltimer to a CSV file
   const char *trace_file = std::getenv("B2C_TRACE_FILE");
   const long long nctas = tc.grid * tc.splits * tc.grid_z;
   unsigned long long *trace = nullptr;
-  if (trace_file && cudaMalloc(&trace, sizeof(unsigned long long) * 3 * nctas) == cudaSuccess) p.trace = trace;
+  if (trace_file && cudaMalloc(&trace, sizeof(unsigned long long) * 5 * nctas) == cudaSuccess) p.trace = trace;
   void *args[] = {&p};
   note_launch();
-  cudaError_t err = cudaLaunchKernel(f.kernel, grid, dim3(tc.threads), args, (size_t)tc.smem_bytes, stream);
+  cudaError_t err;
+  if (p.pdl) {
+    // programmatic dependent launch: this grid's prologue may overlap the tail of
+    // the previous kernel on the stream (the kernel waits before reading inputs)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(tc.threads);
+    cfg.dynamicSmemBytes = (size_t)tc.smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    err = cudaLaunchKernelExC(&cfg, f.kernel, args);
+  } else {
+    err = cudaLaunchKernel(f.kernel, grid, dim3(tc.threads), args, (size_t)tc.smem_bytes, stream);
+  }
+  if (err == cudaSuccess && tc.splits > 1 && !stage1)
+    err = launch_stage2(p.partials, y, p.part_stride, tc.splits, dev, stream);
   if (trace) {
-    std::vector<unsigned long long> h(3 * nctas);
+    std::vector<unsigned long long> h(5 * nctas);
     cudaStreamSynchronize(stream);
     cudaMemcpy(h.data(), trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(trace);
     if (FILE *fp = std::fopen(trace_file, "a")) {
       for (long long i = 0; i < nctas; i++)
-        std::fprintf(fp, "%s,%lld,%llu,%llu,%llu\n", f.name, i, h[3 * i], h[3 * i + 1], h[3 * i + 2]);
+        std::fprintf(fp, "%s,%lld,%llu,%llu,%llu,%llu,%llu\n", f.name, i, h[5 * i], h[5 * i + 1], h[5 * i + 2],
+                     h[5 * i + 3], h[5 * i + 4]);
       std::fclose(fp);
     }
   }
@@ -326,8 +466,17 @@ cudaError_t launch_stage2(const float *partials, float *y, long long total, int 
   long long blocks = std::min<long long>(cdiv(work, 256), (long long)sms * 8);
   if (blocks < 1) blocks = 1;
   note_launch();
-  stage2_sum_kernel<<<(unsigned)blocks, 256, 0, stream>>>(partials, y, total, taps);
-  return cudaGetLastError();
+  const int pdl = pdl_enabled() ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, stage2_sum_kernel, partials, y, total, taps, pdl);
 }
 
 }  // namespace b2c

@@ -103,8 +103,7 @@ class ConvLayer:
             ws_ptr, ws_len = None, 0
             if self.split_workspace_bytes:
                 if self._split_ws is None or self._split_ws.device != x.device:
-                    # zero-filled once; every completed launch leaves it zeroed
-                    self._split_ws = torch.zeros(self.split_workspace_bytes, dtype=torch.uint8, device=x.device)
+                    self._split_ws = torch.empty(self.split_workspace_bytes, dtype=torch.uint8, device=x.device)
                 ws_ptr, ws_len = self._split_ws.data_ptr(), self.split_workspace_bytes
             st = self._lib.b2c_conv2d_forward(ctypes.byref(self._desc), x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                               ws_ptr, ws_len, ctypes.byref(self._tiles), ctypes.c_void_p(s))
