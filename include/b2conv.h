@@ -96,10 +96,29 @@ typedef struct {
 typedef enum {
   B2C_ENGINE_FUSED = 0,    /* single-pass FFMA2 direct convolution, no workspace,
                               within tol(K) = 1e-5*max(1,K/4096) of conv_naive_f64 */
-  B2C_ENGINE_TWOSTAGE = 1  /* paper-faithful stage 1 + stage 2 with the
+  B2C_ENGINE_TWOSTAGE = 1, /* paper-faithful stage 1 + stage 2 with the
                               reference's separate-rounding order: bitwise equal
                               to conv_naive / conv_twostage                      */
+  B2C_ENGINE_TF32X3 = 2,   /* tcgen05 tensor-core implicit GEMM, 3xTF32 operand
+                              splitting (fp32-class: within tol(K) like FUSED)   */
+  B2C_ENGINE_TF32 = 3      /* tcgen05 implicit GEMM, plain TF32 operands
+                              (its own tolerance: 5e-3 relative)                 */
 } b2c_engine;
+
+/* Tile plan of the tensor-core engines (no reference analogue). */
+typedef struct {
+  int32_t pixels_per_chunk; /* chunk width (32, 16, 8): a chunk is 32 output
+                               pixels = (32/width) rows x width columns      */
+  int32_t filters_per_tile; /* UMMA N: output channels per CTA                */
+  int32_t filter_tiles;
+  int32_t stages;           /* TMA/mbarrier pipeline depth                     */
+  int32_t smem_bytes;
+  int32_t tmem_columns;
+  int32_t flattened;        /* 1x1 layers: pixels flattened over the plane     */
+  int32_t passes;           /* 3 (3xTF32) or 1 (TF32)                          */
+  int64_t grid;             /* CTAs (128 output pixels x filters_per_tile each) */
+  int64_t workspace_bytes;  /* filter re-layout buffer ([tap][m][c], 0 if none) */
+} b2c_tc_plan;
 
 /* ---------------------------------------------------------------- metadata */
 int32_t b2c_abi_version(void);
@@ -153,6 +172,19 @@ b2c_status b2c_register_tuned_plan(const b2c_conv_desc *d, int32_t engine, int32
  * summation order is a function of (c, hf, wf, splits) only. */
 b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
                               int64_t workspace_size, const b2c_tile_plan *tiles, void *stream);
+
+/* Tensor-core forward convolution (engine B2C_ENGINE_TF32X3 or _TF32) for
+ * device-resident tensors, any stride and padding.  Same semantics and
+ * output as b2c_conv2d_forward (which it complements for the
+ * large-channel layers, BASELINE.json north star "optional TF32 tcgen05
+ * implicit-GEMM variant").  `workspace` holds the filter re-layout
+ * (b2c_tc_select_tiles().workspace_bytes; NULL when that is 0).  Returns
+ * B2C_UNSUPPORTED for layers beyond its 32-bit per-image offsets. */
+b2c_status b2c_conv2d_forward_tc(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
+                                 int64_t workspace_size, int32_t engine, void *stream);
+/* The tensor-core planner's choice for d (B2C_UNSUPPORTED if not covered).
+ * If out->filters_per_tile > 0 on entry it is forced. */
+b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_plan *out);
 
 /* twostage.conv_twostage (twostage.py:208-239): preconditions in the
  * reference's order, then stage 1 (+ stage 2 unless 1x1) with the reference's

@@ -18,7 +18,8 @@ from .errors import (ConvKitError, DeviceError, InvalidConfig, InvalidPlan, Shap
 LIB_PATH = Path(__file__).resolve().parent / "libb2conv.so"
 
 OK, UNSUPPORTED, SHAPE_MISMATCH, INVALID_PLAN, WORKSPACE_EXCEEDED, INVALID_CONFIG, CUDA_ERROR, INVALID_ARGUMENT = range(8)
-ENGINE_FUSED, ENGINE_TWOSTAGE = 0, 1
+ENGINE_FUSED, ENGINE_TWOSTAGE, ENGINE_TF32X3, ENGINE_TF32 = 0, 1, 2, 3
+ENGINES = {"fused": ENGINE_FUSED, "twostage": ENGINE_TWOSTAGE, "tf32x3": ENGINE_TF32X3, "tf32": ENGINE_TF32}
 FIELD_NAMES = ("n", "c", "h", "w", "m", "hf", "wf", "stride", "pad_h", "pad_w")
 
 
@@ -49,6 +50,13 @@ class TilePlanC(ctypes.Structure):
                 ("workspace_bytes", ctypes.c_int64)]
 
 
+class TcPlanC(ctypes.Structure):
+    _fields_ = [("pixels_per_chunk", ctypes.c_int32), ("filters_per_tile", ctypes.c_int32),
+                ("filter_tiles", ctypes.c_int32), ("stages", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
+                ("tmem_columns", ctypes.c_int32), ("flattened", ctypes.c_int32), ("passes", ctypes.c_int32),
+                ("grid", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64)]
+
+
 _P = ctypes.POINTER
 _fp = ctypes.c_void_p  # raw float* (device or host address)
 
@@ -71,6 +79,9 @@ SIGNATURES = {
     "b2c_register_tuned_plan": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     "b2c_conv2d_forward": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, ctypes.c_void_p, ctypes.c_int64,
                                           _P(TilePlanC), ctypes.c_void_p]),
+    "b2c_conv2d_forward_tc": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, ctypes.c_void_p, ctypes.c_int64,
+                                             ctypes.c_int32, ctypes.c_void_p]),
+    "b2c_tc_select_tiles": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, _P(TcPlanC)]),
     "b2c_conv_twostage": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _fp, ctypes.c_int64, _P(LaunchPlanC),
                                          _P(DeviceModelC), ctypes.c_int64, ctypes.c_void_p, _P(RunStatsC)]),
     "b2c_stage1_scalar_prods": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _P(LaunchPlanC), _P(DeviceModelC),

@@ -16,8 +16,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libb2conv.so"
-SOURCES = [CSRC / "conv_launch.cu", CSRC / "probe.cu", CSRC / "api.cpp"]
-DEPS = SOURCES + [CSRC / "conv_kernel.cuh", CSRC / "conv1x1_vec.cuh", CSRC / "internal.h", ROOT / "include" / "b2conv.h"]
+SOURCES = [CSRC / "conv_launch.cu", CSRC / "conv_tc.cu", CSRC / "probe.cu", CSRC / "api.cpp"]
+DEPS = SOURCES + [CSRC / "conv_kernel.cuh", CSRC / "conv1x1_vec.cuh", CSRC / "conv_tc.cuh", CSRC / "internal.h", ROOT / "include" / "b2conv.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # No --use_fast_math / -ftz: denormals and IEEE rounding must match numpy.

@@ -27,6 +27,26 @@ struct TileChoice {
   double cost = 0;
 };
 
+// Tensor-core implicit-GEMM plan (conv_tc.cu / conv_tc.cuh).
+struct TcPlan {
+  int xb = 0;        // chunk width XW in output columns (32, 16 or 8; chunk = 32/XW rows)
+  int nf = 0;        // output channels per tile (UMMA N)
+  int mtiles = 0;
+  int stages = 0, stage_bytes = 0, smem_bytes = 0, tmem_cols = 0;
+  int passes = 3;    // 3: 3xTF32 (fp32-class), 1: TF32
+  bool flat = false; // 1x1: pixels flattened over the plane
+  long long nchunks = 0;
+  long long grid = 0;
+  double cost = 0;
+};
+bool tc_supported(const Geom &g);
+bool tc_flat(const Geom &g);
+bool tc_needs_relayout(const Geom &g, const float *w);
+long long tc_workspace_bytes(const Geom &g);
+bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, TcPlan *out);
+cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const float *w, float *y, void *workspace,
+                      long long ws_bytes, cudaStream_t stream);
+
 // split-C workspace: `splits` partial planes in the output layout, [split][n][m][ho][wo]
 
 const char *family_name(int id);

@@ -56,8 +56,9 @@ def _check_tensor(t, what: str) -> None:
 class ConvLayer:
     """A resolved forward convolution for one configuration."""
 
-    def __init__(self, cfg: ConvConfig, engine: str = "fused", family: int = -1, splits: int = 0):
-        if engine not in ("fused", "twostage"):
+    def __init__(self, cfg: ConvConfig, engine: str = "fused", family: int = -1, splits: int = 0,
+                 filters_per_tile: int = 0):
+        if engine not in nat.ENGINES:
             raise ValueError(f"unknown engine {engine!r}")
         if engine == "twostage" and cfg.stride != 1:
             raise Unsupported(f"two-stage convolution requires stride 1, got {cfg.stride}")
@@ -68,10 +69,19 @@ class ConvLayer:
         self._tiles = nat.TilePlanC()
         self._tiles.family = int(family)
         self._tiles.splits = int(splits)
-        e = nat.ENGINE_TWOSTAGE if engine == "twostage" else nat.ENGINE_FUSED
-        nat.check(self._lib.b2c_select_tiles(ctypes.byref(self._desc), e, ctypes.byref(self._tiles)))
+        self._engine_id = nat.ENGINES[engine]
+        self.tensor_core = engine in ("tf32x3", "tf32")
+        if self.tensor_core:
+            self._tc = nat.TcPlanC()
+            self._tc.filters_per_tile = int(filters_per_tile)
+            nat.check(self._lib.b2c_tc_select_tiles(ctypes.byref(self._desc), self._engine_id, ctypes.byref(self._tc)))
+        else:
+            e = nat.ENGINE_TWOSTAGE if engine == "twostage" else nat.ENGINE_FUSED
+            nat.check(self._lib.b2c_select_tiles(ctypes.byref(self._desc), e, ctypes.byref(self._tiles)))
         self.out_hw = output_dims(cfg)
         self.workspace_bytes = 0
+        if self.tensor_core:
+            self.workspace_bytes = int(self._tc.workspace_bytes)
         if engine == "twostage" and not (cfg.hf == 1 and cfg.wf == 1):
             self.workspace_bytes = int(self._lib.b2c_workspace_bytes(ctypes.byref(self._desc)))
         self._ws = None
@@ -80,11 +90,14 @@ class ConvLayer:
 
     @property
     def family(self) -> str:
+        if self.tensor_core:
+            t = self._tc
+            return f"{self.engine}_x{t.pixels_per_chunk}_n{t.filters_per_tile}_s{t.stages}" + ("_flat" if t.flattened else "")
         return self._lib.b2c_family_name(self._tiles.family).decode()
 
     @property
     def grid(self) -> int:
-        return int(self._tiles.grid)
+        return int(self._tc.grid if self.tensor_core else self._tiles.grid)
 
     @property
     def splits(self) -> int:
@@ -107,6 +120,13 @@ class ConvLayer:
                 ws_ptr, ws_len = self._split_ws.data_ptr(), self.split_workspace_bytes
             st = self._lib.b2c_conv2d_forward(ctypes.byref(self._desc), x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                               ws_ptr, ws_len, ctypes.byref(self._tiles), ctypes.c_void_p(s))
+            nat.check(st)
+        elif self.tensor_core:
+            if self.workspace_bytes and (self._ws is None or self._ws.device != x.device):
+                self._ws = torch.empty(self.workspace_bytes // 4, dtype=torch.float32, device=x.device)
+            ws_ptr = self._ws.data_ptr() if self.workspace_bytes else None
+            st = self._lib.b2c_conv2d_forward_tc(ctypes.byref(self._desc), x.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                                 ws_ptr, self.workspace_bytes, self._engine_id, ctypes.c_void_p(s))
             nat.check(st)
         else:
             if self.workspace_bytes and (self._ws is None or self._ws.device != x.device):

@@ -19,6 +19,12 @@ Two engines sit behind the same call:
     registers, no workspace (so ``workspace_limit`` never trips), within
     tol(K) = 1e-5*max(1, K/4096) of ``conv_naive_f64`` (K = c*hf*wf).
 
+``engine="tf32x3"`` / ``engine="tf32"``
+    The optional tensor-core variant (tcgen05 implicit GEMM, TMA-shifted
+    input rows, TMEM accumulators): 3xTF32 operand splitting is fp32-class
+    (within tol(K)); plain TF32 has its own 5e-3 tolerance.  Stride 1 and
+    W % 4 == 0 (or unpadded 1x1 with H*W % 4 == 0) only: Unsupported otherwise.
+
 ``workers`` is accepted for signature compatibility; the GPU result is
 independent of it (as the reference's is).
 """
@@ -37,7 +43,7 @@ from .execmodel import DeviceModel, LaunchPlan, plan_launch, validate_plan
 from .tensor import Tensor4
 
 DEFAULT_WORKSPACE_LIMIT = 1_073_741_824
-ENGINES = ("twostage", "fused")
+ENGINES = ("twostage", "fused", "tf32x3", "tf32")
 
 
 def workspace_bytes(cfg: ConvConfig) -> int:
@@ -117,12 +123,12 @@ def conv_twostage(inp: Tensor4, filters: Tensor4, cfg: ConvConfig, device: Devic
     ho, wo = output_dims(cfg)
     out = np.empty((cfg.n, cfg.m, ho, wo), dtype=np.float32)
     stats = nat.RunStatsC()
-    e = nat.ENGINE_TWOSTAGE if engine == "twostage" else nat.ENGINE_FUSED
+    e = nat.ENGINES[engine]
     st = nat.lib().b2c_conv_host(ctypes.byref(nat.desc(cfg)), inp.data.ctypes.data, filters.data.ctypes.data,
                                  out.ctypes.data, e, ctypes.byref(plan._c()), ctypes.byref(device._c()),
                                  int(workspace_limit), int(gpu), ctypes.byref(stats))
     nat.check(st, required=required, limit=workspace_limit)
-    if engine == "fused":
+    if engine != "twostage":
         return Tensor4(out), RunStats(plan.blocks, False, plan.blocks, 0)
     return Tensor4(out), _stats(stats)
 
@@ -165,7 +171,8 @@ def stage2_sum(partials: PartialSums, cfg: ConvConfig, *, workers: int = 1,
     return Tensor4(out), RunStats(stage2_invoked=True)
 
 
-def conv_forward(inp: Tensor4, filters: Tensor4, cfg: ConvConfig, *, gpu: int = -1) -> Tensor4:
+def conv_forward(inp: Tensor4, filters: Tensor4, cfg: ConvConfig, *, gpu: int = -1,
+                 engine: str = "fused") -> Tensor4:
     """Fused-engine convolution for any stride >= 1 and any padding (the
     operand contract of reference.conv_naive, reference.py:58-83), host in /
     host out."""
@@ -173,6 +180,6 @@ def conv_forward(inp: Tensor4, filters: Tensor4, cfg: ConvConfig, *, gpu: int = 
     ho, wo = output_dims(cfg)
     out = np.empty((cfg.n, cfg.m, ho, wo), dtype=np.float32)
     st = nat.lib().b2c_conv_host(ctypes.byref(nat.desc(cfg)), inp.data.ctypes.data, filters.data.ctypes.data,
-                                 out.ctypes.data, nat.ENGINE_FUSED, None, None, 0, int(gpu), None)
+                                 out.ctypes.data, nat.ENGINES[engine], None, None, 0, int(gpu), None)
     nat.check(st)
     return Tensor4(out)
