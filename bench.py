@@ -20,6 +20,10 @@ per-layer CUDA-event timings, over the FFMA2 peak measured live by
 reference's conv_twostage on the host's cores), ``clocks`` (NVML during the
 timed region) and ``gpu_launches``.
 
+``tensor_core_variant``: the north star's optional tcgen05 implicit-GEMM
+engine (3xTF32 by default, ``--tc-engine``) on the same workload and operands,
+with its own stated tolerance and a tensor-bound roofline.
+
 ``--impl reference`` times the reference algorithm on the CPU (the oracle
 port of convkit.conv_twostage, all host threads) for the same metric/config;
 under torchrun only rank 0 runs it.
@@ -53,7 +57,9 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5"), default="c2")
     ap.add_argument("--batch", type=int, default=0, help="images per layer (per GPU, or global for c5)")
-    ap.add_argument("--engine", choices=("fused", "twostage"), default="fused")
+    ap.add_argument("--engine", choices=("fused", "twostage", "tf32x3", "tf32"), default="fused")
+    ap.add_argument("--tc-engine", choices=("tf32x3", "tf32", "none"), default="tf32x3",
+                    help="tensor-core variant reported separately in the same line (north star: optional, own tolerance)")
     ap.add_argument("--report", default="", help="write a per-layer sweep of every BASELINE config to PATH")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -242,7 +248,9 @@ def sweep_report(path, device, peak_tflops):
             layers = [ConvLayer(c, "fused") for c in cfgs]
             xs, ws, ys = make_operands(cfgs, device, 1)
             ms = time_layers(layers, xs, ws, ys, reps=10)
-            for c, L, t in zip(cfgs, layers, ms):
+            tcl = [ConvLayer(c, "tf32x3") for c in cfgs]
+            tms = time_layers(tcl, xs, ws, ys, reps=10)
+            for c, L, t, T, tt in zip(cfgs, layers, ms, tcl, tms):
                 flop_per_byte = c.flops / c.compulsory_bytes
                 ridge = peak_tflops * 1e12 / (hbm * 1e9)
                 if flop_per_byte >= ridge:
@@ -252,12 +260,140 @@ def sweep_report(path, device, peak_tflops):
                 rows.append({"workload": wl, "batch": n, "layer": c.name, "c": c.c, "hw": c.h, "m": c.m,
                              "f": c.hf, "stride": c.stride, "us": round(t * 1e3, 2),
                              "gflops": round(c.flops / (t * 1e-3) / 1e9, 1), "bound": bound,
-                             "roofline_frac": round(frac, 4), "family": L.family, "grid": L.grid})
+                             "roofline_frac": round(frac, 4), "family": L.family, "grid": L.grid,
+                             "tf32x3_us": round(tt * 1e3, 2), "tf32x3_gflops": round(c.flops / (tt * 1e-3) / 1e9, 1),
+                             "tf32x3_plan": T.family})
             del xs, ws, ys
             torch.cuda.empty_cache()
     with open(path, "w") as fh:
         json.dump({"peak_fp32_tflops": peak_tflops, "hbm_gbs": hbm, "rows": rows}, fh, indent=1)
     return rows
+
+
+def time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank):
+    """Warm up, capture one step (every layer once) as a CUDA graph, then time
+    exactly `steps` replays between barriers + synchronize (CUDA events on
+    the replay stream, max over ranks).  Returns (ms, launches/step, clocks)."""
+    import torch
+    import torch.distributed as dist
+
+    def step():
+        for L, x, w, y in zip(layers, xs, ws, ys):
+            L(x, w, out=y)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    cap_stream = torch.cuda.Stream()
+    with torch.cuda.stream(cap_stream):
+        step()  # warm on the capture stream (allocates per-layer workspaces)
+        torch.cuda.synchronize()
+        lib.b2c_reset_launch_count()
+        with torch.cuda.graph(graph, stream=cap_stream):
+            step()
+    launches_per_step = int(lib.b2c_launch_count())
+    for _ in range(max(args.warmup, 3)):
+        graph.replay()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        start.record()
+        for _ in range(args.steps):
+            graph.replay()
+        end.record()
+        torch.cuda.synchronize()
+    ms_local = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms_local], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        return float(t.item()), launches_per_step, clk
+    return ms_local, launches_per_step, clk
+
+
+def e2e_run(lib, nat, cfgs, xs, ws, ys, engine_id, steps, world, device, local_rank):
+    """Same metric through the host-buffer C-ABI drop-in: every step copies each
+    layer's input and filters from pinned host memory, convolves, and copies
+    the output back (synchronous per layer).  Wall time, max over ranks."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    pinned = []
+    h2d = d2h = 0
+    for c, x, w, y in zip(cfgs, xs, ws, ys):
+        hx = torch.empty(x.shape, dtype=torch.float32, pin_memory=True).copy_(x)
+        hw = torch.empty(w.shape, dtype=torch.float32, pin_memory=True).copy_(w)
+        hy = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+        pinned.append((nat.desc(c), hx, hw, hy))
+        h2d += hx.numel() * 4 + hw.numel() * 4
+        d2h += hy.numel() * 4
+
+    def e2e_step():
+        for d, hx, hw, hy in pinned:
+            nat.check(lib.b2c_conv_host(ctypes.byref(d), hx.data_ptr(), hw.data_ptr(), hy.data_ptr(), engine_id,
+                                        None, None, 1 << 62, local_rank, None))
+
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        e2e_step()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    flops = sum(c.flops for c in cfgs)
+    return {"value": round(flops * world * steps / dt / 1e9, 3), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+            "ms_per_step": round(1e3 * dt / steps, 3),
+            "path": "b2c_conv_host (C ABI, pinned host buffers, synchronous per layer)"}
+
+
+TC_TOLERANCE = {"tf32x3": "relative_error vs conv_naive_f64 <= 1e-5*max(1, K/4096) (the fp32 gate)",
+                "tf32": "relative_error vs conv_naive_f64 <= 5e-3"}
+
+
+def tensor_core_variant(args, lib, nat, cfgs, xs, ws, ys, world, device, local_rank):
+    """The north star's optional tcgen05 implicit-GEMM variant on the same
+    workload and operands, reported separately with its stated tolerance.
+    Roofline: tensor-bound against the tf32 dense rate, taken as half the
+    measured cuBLAS bf16 burst rate (MEASURED_PEAKS.json; B200 dense
+    tf32:bf16 = 1:2), divided by 3 for 3xTF32 (three tf32 MMAs per product)."""
+    from paper_2103_16234_b200 import ConvLayer
+
+    eng = args.tc_engine
+    layers = [ConvLayer(c, eng) for c in cfgs]
+    ms_total, launches, clk = time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank)
+    flops = sum(c.flops for c in cfgs)
+    layer_ms = time_layers(layers, xs, ws, ys)
+    kern_ms = sum(layer_ms)
+    pk = peaks()
+    tf32_peak = pk.get("bf16_tflops", 1590.0) / 2.0
+    passes = 3 if eng == "tf32x3" else 1
+    achieved = flops / (kern_ms * 1e-3) / 1e12
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e = e2e_run(lib, nat, cfgs, xs, ws, ys, nat.ENGINES[eng], args.e2e_steps, world, device, local_rank)
+    return {"engine": eng, "value": round(flops * world * args.steps / (ms_total * 1e-3) / 1e9, 3),
+            "unit": "GFLOP/s", "ms_per_step": round(ms_total / args.steps, 4), "tolerance": TC_TOLERANCE[eng],
+            "dtype": "tf32x3 (fp32 operands split hi+lo, fp32 accumulate in TMEM)" if passes == 3 else "tf32",
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 3),
+                         "peak": round(tf32_peak / passes, 3), "unit": "TFLOP/s",
+                         "frac": round(achieved * passes / tf32_peak, 4), "traffic": None,
+                         "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (dense tf32 rate)"
+                                         + (" / 3 (3xTF32)" if passes == 3 else "")),
+                         "kernel_ms_per_step": round(kern_ms, 4)},
+            "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches * args.steps,
+            "per_layer": [{"layer": c.name, "us": round(t * 1e3, 2), "gflops": round(c.flops / (t * 1e-3) / 1e9, 1),
+                           "plan": L.family} for c, L, t in zip(cfgs, layers, layer_ms)]}
 
 
 def main():
@@ -302,51 +438,10 @@ def main():
 
     layers = [ConvLayer(c, args.engine) for c in cfgs]
     xs, ws, ys = make_operands(cfgs, device, 1234 + rank)
-
-    def step():
-        for L, x, w, y in zip(layers, xs, ws, ys):
-            L(x, w, out=y)
-
-    for _ in range(max(args.warmup, 1)):
-        step()
-    torch.cuda.synchronize()
-    # capture one step as a CUDA graph (launch-bound 36-layer pass)
-    graph = torch.cuda.CUDAGraph()
-    lib.b2c_reset_launch_count()
-    cap_stream = torch.cuda.Stream()
-    with torch.cuda.stream(cap_stream):
-        step()  # warm on the capture stream
-        torch.cuda.synchronize()
-        lib.b2c_reset_launch_count()
-        with torch.cuda.graph(graph, stream=cap_stream):
-            step()
-    launches_per_step = int(lib.b2c_launch_count())
-    for _ in range(max(args.warmup, 3)):
-        graph.replay()
-    torch.cuda.synchronize()
-
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
-        start.record()
-        for _ in range(args.steps):
-            graph.replay()
-        end.record()
-        torch.cuda.synchronize()
-    ms_local = start.elapsed_time(end)
-    if world > 1:
-        t = torch.tensor([ms_local], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
-        ms_total = float(t.item())
-    else:
-        ms_total = ms_local
+    ms_total, launches_per_step, clk = time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank)
     flops_step_rank = sum(c.flops for c in cfgs)
     value = flops_step_rank * world * args.steps / (ms_total * 1e-3) / 1e9
     ms_per_step = ms_total / args.steps
-
     # per-layer kernel times -> roofline of the conv kernel family
     layer_ms = time_layers(layers, xs, ws, ys)
     kern_ms = sum(layer_ms)
@@ -359,38 +454,13 @@ def main():
     # e2e: host buffers through the C-ABI drop-in (H2D x,w + kernel + D2H y per layer)
     e2e = None
     if args.e2e_steps > 0:
-        import ctypes
-        pinned = []
-        h2d = d2h = 0
-        for c, x, w, y in zip(cfgs, xs, ws, ys):
-            hx = torch.empty(x.shape, dtype=torch.float32, pin_memory=True).copy_(x)
-            hw = torch.empty(w.shape, dtype=torch.float32, pin_memory=True).copy_(w)
-            hy = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
-            pinned.append((nat.desc(c), hx, hw, hy))
-            h2d += hx.numel() * 4 + hw.numel() * 4
-            d2h += hy.numel() * 4
+        e2e = e2e_run(lib, nat, cfgs, xs, ws, ys, nat.ENGINES[args.engine], args.e2e_steps, world, device,
+                      local_rank)
 
-        def e2e_step():
-            for d, hx, hw, hy in pinned:
-                nat.check(lib.b2c_conv_host(ctypes.byref(d), hx.data_ptr(), hw.data_ptr(), hy.data_ptr(),
-                                            nat.ENGINE_FUSED if args.engine == "fused" else nat.ENGINE_TWOSTAGE,
-                                            None, None, 1 << 62, local_rank, None))
-
-        e2e_step()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            e2e_step()
-        dt = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([dt], device=device, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
-        e2e = {"value": round(flops_step_rank * world * args.e2e_steps / dt / 1e9, 3), "unit": "GFLOP/s",
-               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-               "ms_per_step": round(1e3 * dt / args.e2e_steps, 3),
-               "path": "b2c_conv_host (C ABI, pinned host buffers, synchronous per layer)"}
+    # the optional tensor-core variant (tcgen05 implicit GEMM), reported separately
+    tc = None
+    if args.tc_engine != "none" and args.engine not in ("tf32x3", "tf32"):
+        tc = tensor_core_variant(args, lib, nat, cfgs, xs, ws, ys, world, device, local_rank)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -421,7 +491,7 @@ def main():
                              "kernel_ms_per_step": round(kern_ms, 4)},
                 "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
                 "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
-                "per_layer": per_layer}
+                "per_layer": per_layer, "tensor_core_variant": tc}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -116,8 +116,14 @@ typedef struct {
   int32_t tmem_columns;
   int32_t flattened;        /* 1x1 layers: pixels flattened over the plane     */
   int32_t passes;           /* 3 (3xTF32) or 1 (TF32)                          */
-  int64_t grid;             /* CTAs (128 output pixels x filters_per_tile each) */
-  int64_t workspace_bytes;  /* filter re-layout buffer ([tap][m][c], 0 if none) */
+  int64_t grid;             /* CTAs (128 output pixels x filters_per_tile each,
+                               times splits)                                  */
+  int32_t splits;           /* split-K over (16-channel block, tap) k-blocks;
+                               partial planes summed by a second launch      */
+  int64_t workspace_bytes;  /* pre-tiled filters (4*ceil(c/16)*16*hf*wf*filter_tiles
+                               *filters_per_tile*passes' planes, rounded up to
+                               256) + split-K partials (4*splits*n*m*ho*wo
+                               when splits > 1)                               */
 } b2c_tc_plan;
 
 /* ---------------------------------------------------------------- metadata */
@@ -177,13 +183,15 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
  * device-resident tensors, any stride and padding.  Same semantics and
  * output as b2c_conv2d_forward (which it complements for the
  * large-channel layers, BASELINE.json north star "optional TF32 tcgen05
- * implicit-GEMM variant").  `workspace` holds the filter re-layout
- * (b2c_tc_select_tiles().workspace_bytes; NULL when that is 0).  Returns
+ * implicit-GEMM variant").  `workspace` receives the per-call pre-tiled
+ * filters and the split-K partial planes (b2c_tc_select_tiles()
+ * .workspace_bytes bytes).  `tiles` may be NULL (planner's choice) or force
+ * filters_per_tile / splits (0 = planner's choice).  Returns
  * B2C_UNSUPPORTED for layers beyond its 32-bit per-image offsets. */
 b2c_status b2c_conv2d_forward_tc(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
-                                 int64_t workspace_size, int32_t engine, void *stream);
+                                 int64_t workspace_size, int32_t engine, const b2c_tc_plan *tiles, void *stream);
 /* The tensor-core planner's choice for d (B2C_UNSUPPORTED if not covered).
- * If out->filters_per_tile > 0 on entry it is forced. */
+ * out->filters_per_tile / out->splits > 0 on entry are forced. */
 b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_plan *out);
 
 /* twostage.conv_twostage (twostage.py:208-239): preconditions in the

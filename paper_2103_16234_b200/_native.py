@@ -54,7 +54,7 @@ class TcPlanC(ctypes.Structure):
     _fields_ = [("pixels_per_chunk", ctypes.c_int32), ("filters_per_tile", ctypes.c_int32),
                 ("filter_tiles", ctypes.c_int32), ("stages", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("tmem_columns", ctypes.c_int32), ("flattened", ctypes.c_int32), ("passes", ctypes.c_int32),
-                ("grid", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64)]
+                ("grid", ctypes.c_int64), ("splits", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
 
 
 _P = ctypes.POINTER
@@ -80,7 +80,7 @@ SIGNATURES = {
     "b2c_conv2d_forward": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, ctypes.c_void_p, ctypes.c_int64,
                                           _P(TilePlanC), ctypes.c_void_p]),
     "b2c_conv2d_forward_tc": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, ctypes.c_void_p, ctypes.c_int64,
-                                             ctypes.c_int32, ctypes.c_void_p]),
+                                             ctypes.c_int32, _P(TcPlanC), ctypes.c_void_p]),
     "b2c_tc_select_tiles": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, _P(TcPlanC)]),
     "b2c_conv_twostage": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _fp, ctypes.c_int64, _P(LaunchPlanC),
                                          _P(DeviceModelC), ctypes.c_int64, ctypes.c_void_p, _P(RunStatsC)]),

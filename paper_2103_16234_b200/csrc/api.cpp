@@ -428,13 +428,19 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
 }
 
 namespace {
-b2c_status tc_plan_of(const b2c_conv_desc *d, const b2c::Geom &g, int32_t engine, int forced_nf, b2c::TcPlan *pl) {
+b2c_status tc_plan_of(const b2c_conv_desc *d, const b2c::Geom &g, int32_t engine, int forced_nf, int forced_splits,
+                      b2c::TcPlan *pl) {
   if (engine != B2C_ENGINE_TF32X3 && engine != B2C_ENGINE_TF32)
     return fail(B2C_INVALID_ARGUMENT, "engine %d is not a tensor-core engine", engine);
   if (forced_nf > 0 && (forced_nf % 16 != 0 || forced_nf > 256))
     return fail(B2C_INVALID_PLAN, "filters_per_tile must be a multiple of 16 in [16, 256], got %d", forced_nf);
-  if (!b2c::plan_tc(g, engine == B2C_ENGINE_TF32X3 ? 3 : 1, forced_nf, 0, pl))
+  if (forced_splits < 0 || forced_splits > 64) return fail(B2C_INVALID_PLAN, "splits must be in [0, 64], got %d", forced_splits);
+  if (!b2c::plan_tc(g, engine == B2C_ENGINE_TF32X3 ? 3 : 1, forced_nf, 0, forced_splits, pl)) {
+    if (forced_splits > 0 || forced_nf > 0)
+      return fail(B2C_INVALID_PLAN, "forced tensor-core tile (filters %d, splits %d) cannot run this layer", forced_nf,
+                  forced_splits);
     return fail(B2C_UNSUPPORTED, "layer too large for the tensor-core engine's 32-bit per-image offsets");
+  }
   (void)d;
   return B2C_OK;
 }
@@ -447,7 +453,7 @@ b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_pl
   b2c::Geom g = geom_of(d);
   if ((st = check_sizes(g)) != B2C_OK) return st;
   b2c::TcPlan pl;
-  if ((st = tc_plan_of(d, g, engine, out->filters_per_tile, &pl)) != B2C_OK) return st;
+  if ((st = tc_plan_of(d, g, engine, out->filters_per_tile, out->splits, &pl)) != B2C_OK) return st;
   out->pixels_per_chunk = pl.xb;
   out->filters_per_tile = pl.nf;
   out->filter_tiles = pl.mtiles;
@@ -457,22 +463,24 @@ b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_pl
   out->flattened = pl.flat ? 1 : 0;
   out->passes = pl.passes;
   out->grid = pl.grid;
-  out->workspace_bytes = (g.HF == 1 && g.WF == 1 && g.C % 4 == 0) ? 0 : b2c::tc_workspace_bytes(g);
+  out->splits = pl.splits;
+  out->workspace_bytes = b2c::tc_workspace_bytes(g, pl);
   return B2C_OK;
 }
 
 b2c_status b2c_conv2d_forward_tc(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
-                                 int64_t workspace_size, int32_t engine, void *stream) {
+                                 int64_t workspace_size, int32_t engine, const b2c_tc_plan *tiles, void *stream) {
   b2c_status st = check_config(d, nullptr);
   if (st != B2C_OK) return st;
   if (!x || !w || !y) return fail(B2C_INVALID_ARGUMENT, "null tensor pointer");
   b2c::Geom g = geom_of(d);
   if ((st = check_sizes(g)) != B2C_OK) return st;
   b2c::TcPlan pl;
-  if ((st = tc_plan_of(d, g, engine, 0, &pl)) != B2C_OK) return st;
-  if (b2c::tc_needs_relayout(g, w) && (!workspace || workspace_size < b2c::tc_workspace_bytes(g)))
+  if ((st = tc_plan_of(d, g, engine, tiles ? tiles->filters_per_tile : 0, tiles ? tiles->splits : 0, &pl)) != B2C_OK)
+    return st;
+  if (!workspace || workspace_size < b2c::tc_workspace_bytes(g, pl))
     return fail(B2C_INVALID_ARGUMENT, "tensor-core engine needs a %lld-byte filter workspace, %lld provided",
-                (long long)b2c::tc_workspace_bytes(g), (long long)workspace_size);
+                (long long)b2c::tc_workspace_bytes(g, pl), (long long)workspace_size);
   cudaError_t e = b2c::launch_tc(g, pl, x, w, y, workspace, workspace_size, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "tensor-core conv launch");
   return B2C_OK;
@@ -574,8 +582,8 @@ b2c_status b2c_conv_host(const b2c_conv_desc *d, const float *x_host, const floa
     splitb = (size_t)tc.ws_bytes;
   } else if (tensor_core) {
     b2c::TcPlan pl;
-    if ((st = tc_plan_of(d, g, engine, 0, &pl)) != B2C_OK) return st;
-    splitb = (size_t)b2c::tc_workspace_bytes(g);
+    if ((st = tc_plan_of(d, g, engine, 0, 0, &pl)) != B2C_OK) return st;
+    splitb = (size_t)b2c::tc_workspace_bytes(g, pl);
   }
   if ((st = ensure(*b, 0, xb)) || (st = ensure(*b, 1, wb)) || (st = ensure(*b, 2, yb)) ||
       (wsb && (st = ensure(*b, 3, wsb))) || (splitb && (st = ensure(*b, 4, splitb))))
@@ -590,7 +598,7 @@ b2c_status b2c_conv_host(const b2c_conv_desc *d, const float *x_host, const floa
     st = b2c_conv2d_forward(d, dx, dw, dy, splitb ? b->ptr[4] : nullptr, (int64_t)splitb, nullptr, b->stream);
     if (stats) std::memset(stats, 0, sizeof(*stats));
   } else if (tensor_core) {
-    st = b2c_conv2d_forward_tc(d, dx, dw, dy, b->ptr[4], (int64_t)splitb, engine, b->stream);
+    st = b2c_conv2d_forward_tc(d, dx, dw, dy, b->ptr[4], (int64_t)splitb, engine, nullptr, b->stream);
     if (stats) std::memset(stats, 0, sizeof(*stats));
   } else {
     st = b2c_conv_twostage(d, dx, dw, dy, static_cast<float *>(b->ptr[3]), (int64_t)wsb, &rp, dev,

@@ -1,7 +1,5 @@
-// Host side of the tcgen05 implicit-GEMM engine (conv_tc.cuh): tensor maps,
-// tile planner and launch.  The tensor-map encoder is fetched from the driver
-// through the runtime (cudaGetDriverEntryPoint), so libb2conv.so keeps linking
-// only the static CUDA runtime.
+// Host side of the tcgen05 implicit-GEMM engine (conv_tc.cuh): tile planner,
+// per-call filter pre-tiling and launch.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -19,23 +17,6 @@ namespace b2c {
 
 namespace {
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
-}
-
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 
 const void *tc_kernel(int passes) {
@@ -52,19 +33,20 @@ bool tc_flat(const Geom &g) { return g.HF == 1 && g.WF == 1 && g.S == 1 && g.PH 
 bool tc_supported(const Geom &g) {
   // chunk/tile indices and per-image offsets are 32-bit in the kernel's inner loops
   if ((long long)g.C * g.H * g.W >= (1LL << 31) || (long long)g.M * g.HoWo >= (1LL << 31)) return false;
-  return true;  // the tensor-map encoder (needs a driver) is checked at launch
+  return true;
 }
 
-bool tc_needs_relayout(const Geom &g, const float *w) {
-  return !(g.HF == 1 && g.WF == 1 && g.C % 4 == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0);
+long long tc_filter_bytes(const Geom &g, const TcPlan &pl) {
+  const long long b = 4LL * cdiv(g.C, tc::BC) * tc::BC * g.HF * g.WF * (long long)pl.mtiles * pl.nf * (pl.passes == 3 ? 2 : 1);
+  return (b + 255) / 256 * 256;
 }
 
-long long tc_workspace_bytes(const Geom &g) {
-  const long long cp = (g.C + 3) / 4 * 4;
-  return 4LL * g.HF * g.WF * g.M * cp;
+long long tc_workspace_bytes(const Geom &g, const TcPlan &pl) {
+  const long long partials = pl.splits > 1 ? 4LL * pl.splits * g.N * g.M * g.HoWo : 0;
+  return tc_filter_bytes(g, pl) + partials;
 }
 
-bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, TcPlan *out) {
+bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced_splits, TcPlan *out) {
   if (!tc_supported(g)) return false;
   const bool flat = tc_flat(g);
   const int wo = flat ? g.HoWo : g.Wo;
@@ -92,38 +74,58 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, TcPlan *ou
   const int sms = device_sm_count(0);
   TcPlan best;
   double best_cost = 1e300;
+  // 3xTF32 accuracy: the tensor core accumulates with truncation, so the main
+  // accumulator's error grows with its number of steps; keep <= 1152 products
+  // (72 k-blocks of 16 channels) per split, the split partials being summed in
+  // fp32 round-to-nearest (measured: within tol(K) up to K = 4608 with margin)
+  const int max_kbps = passes == 3 ? 72 : 1 << 30;
+  const double out_bytes = 4.0 * g.N * g.M * g.HoWo;
   for (int mt = 1; mt <= 64; mt++) {
     int nf = (int)cdiv(cdiv(g.M, mt), 16) * 16;
     if (nf > 256) continue;
     if (forced_nf > 0) nf = forced_nf;
     const int mtiles = (int)cdiv(g.M, nf);
-    const long long stage = (long long)(tc::A_BYTES + nf * 64) * (passes == 3 ? 2 : 1);
+    const long long stage = (long long)(tc::A_BYTES + nf * 64) * (passes == 3 ? 2 : 1);  // A + B (+ lo planes)
     const int stages = (int)std::min<long long>(6, (kSmemBudget - 2048) / stage);
     if (stages < 2) continue;
-    const long long ctas = ptiles * mtiles;
-    // per-stage clocks: tensor (128 x nf x 8 UMMA ~ nf/2 clk, >= 16), smem and L2 feeds
-    const double mma = passes * 2.0 * std::max(nf / 2.0, 16.0);
-    const double l2 = (tc::A_BYTES + nf * 64) / 28.0;
-    const double split = passes == 3 ? 2.0 * (tc::A_BYTES + nf * 64) / 128.0 : 0.0;
-    const double t_cta = KB * std::max({mma, l2, split}) + 2500.0 + nf * 4.0;
-    const double cost = (double)cdiv(ctas, sms) * t_cta;
-    if (cost < best_cost) {
-      best_cost = cost;
-      best.xb = xw;
-      best.nf = nf;
-      best.mtiles = mtiles;
-      best.stages = stages;
-      best.stage_bytes = (int)stage;
-      best.grid = ctas;
-      best.passes = passes;
-      best.flat = flat;
-      best.nchunks = nchunks;
+    static const int kAuto[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
+    const int nopt = forced_splits > 0 ? 1 : (int)(sizeof(kAuto) / sizeof(int));
+    for (int oi = 0; oi < nopt; oi++) {
+      const int sp = forced_splits > 0 ? forced_splits : kAuto[oi];
+      if (sp > KB) break;
+      const int kbps = (int)cdiv(KB, sp);
+      const int splits = (int)cdiv(KB, kbps);
+      if (splits != sp && forced_splits <= 0) continue;  // duplicate of a smaller split
+      if (kbps > max_kbps && forced_splits <= 0) continue;
+      const long long ctas = ptiles * mtiles * splits;
+      // per-k-block clocks (B200 measurements): tensor issue ~95 clk per
+      // 128x256x8 tf32 UMMA, and a ~1.1-1.3k clk latency chain per k-block
+      // (barrier hand-offs + loader stores) shared by the two loader groups
+      const double mma = passes * 2.0 * std::max(95.0 * nf / 256.0, 12.0);
+      const double chain = passes == 3 ? 1300.0 : 1100.0;
+      const double t_cta = kbps * std::max(mma, chain) + 6000.0 + nf * 8.0;
+      double cost = (double)cdiv(ctas, sms) * t_cta;
+      if (splits > 1) cost += 4000.0 + 2.0 * (splits + 1) * out_bytes / (3.0e3 * sms / 148.0);  // stage-2 sum
+      if (cost < best_cost) {
+        best_cost = cost;
+        best.xb = xw;
+        best.nf = nf;
+        best.mtiles = mtiles;
+        best.stages = stages;
+        best.stage_bytes = (int)stage;
+        best.grid = ctas;
+        best.passes = passes;
+        best.flat = flat;
+        best.nchunks = nchunks;
+        best.splits = splits;
+        best.kb_per_split = kbps;
+      }
     }
     if (forced_nf > 0) break;
   }
   if (best.nf == 0) return false;
   int cols = 32;
-  while (cols < best.nf) cols <<= 1;
+  while (cols < best.nf * (passes == 3 ? 2 : 1)) cols <<= 1;  // 3xTF32: main + correction accumulators
   best.tmem_cols = cols;
   best.smem_bytes = best.stages * best.stage_bytes + 1024 /*align*/ + 256 /*barriers*/;
   best.cost = best_cost;
@@ -133,36 +135,26 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, TcPlan *ou
 
 cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const float *w, float *y, void *workspace,
                       long long ws_bytes, cudaStream_t stream) {
-  EncodeTiledFn enc = encode_fn();
-  if (!enc) return cudaErrorNotSupported;
-  const float *wsrc = w;
-  int cp = g.C;
   const int taps = g.HF * g.WF;
-  if (tc_needs_relayout(g, w)) {
-    cp = (g.C + 3) / 4 * 4;
-    if (!workspace || ws_bytes < tc_workspace_bytes(g)) return cudaErrorInvalidValue;
-    float *wp = static_cast<float *>(workspace);
-    const long long total = (long long)taps * g.M * cp;
-    const int blocks = (int)std::min<long long>(cdiv(total, 256), 4LL * device_sm_count(0));
+  const int cblocks = (int)cdiv(g.C, tc::BC);
+  const int Mp = pl.mtiles * pl.nf;
+  if (!workspace || ws_bytes < tc_workspace_bytes(g, pl)) return cudaErrorInvalidValue;
+  float *wt = static_cast<float *>(workspace);
+  const int planes = pl.passes == 3 ? 2 : 1;
+  {
+    const long long total = (long long)cblocks * taps * Mp * tc::BC * planes;
+    const int blocks = (int)std::min<long long>(cdiv(total, 256), 8LL * device_sm_count(0));
     note_launch();
-    tc::filter_relayout_kernel<<<blocks, 256, 0, stream>>>(w, wp, g.M, g.C, cp, taps);
+    tc::filter_tile_kernel<<<blocks, 256, 0, stream>>>(w, wt, g.M, g.C, taps, pl.nf, pl.mtiles, cblocks, planes);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    wsrc = wp;
   }
+  const int rc = 32 / pl.xb;
 
   tc::TcParams p;
   std::memset(&p, 0, sizeof(p));
-  cuuint32_t ones[4] = {1, 1, 1, 1};
-  const int rc = 32 / pl.xb;
-  cuuint64_t wdim[3] = {(cuuint64_t)cp, (cuuint64_t)g.M, (cuuint64_t)taps};
-  cuuint64_t wstr[2] = {(cuuint64_t)cp * 4, (cuuint64_t)cp * g.M * 4};
-  cuuint32_t wbox[3] = {(cuuint32_t)tc::BC, (cuuint32_t)pl.nf, 1};
-  CUresult r = enc(&p.wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(wsrc), wdim, wstr, wbox, ones,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-
+  p.wt = wt;
+  p.Mp = Mp;
   p.x = x;
   p.y = y;
   p.C = g.C;
@@ -188,13 +180,20 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   p.mtiles = pl.mtiles;
   p.cblocks = (int)cdiv(g.C, tc::BC);
   p.stages = pl.stages;
-  p.b_bytes = pl.nf * 64;
+  p.b_bytes = pl.nf * 64 * planes;
   p.stage_bytes = pl.stage_bytes;
   p.tmem_cols = pl.tmem_cols;
-  // kind::tf32 instruction descriptor: D f32, A/B tf32, A MN-major (pixels), B K-major (filters)
-  p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | ((uint32_t)(pl.nf >> 3) << 17) |
+  p.splits = pl.splits;
+  p.kb_per_split = pl.kb_per_split;
+  if (pl.splits > 1) {
+    p.partials = reinterpret_cast<float *>(static_cast<char *>(workspace) + tc_filter_bytes(g, pl));
+    p.part_stride = (long long)g.N * g.M * g.HoWo;
+  }
+  // kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major
+  p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(pl.nf >> 3) << 17) |
             ((uint32_t)(tc::TILE_P >> 4) << 24);
   p.spin_limit = 4000000000ull;  // 4 s
+  if (const char *m = std::getenv("B2C_TC_MODE")) p.mode = std::atoi(m);
 
   const void *kern = tc_kernel(pl.passes);
   static std::mutex mu;
@@ -204,7 +203,7 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)pl.grid);
+  cfg.gridDim = dim3((unsigned)(pl.grid / pl.splits), (unsigned)pl.splits);
   cfg.blockDim = dim3(tc::THREADS);
   cfg.dynamicSmemBytes = (size_t)pl.smem_bytes;
   cfg.stream = stream;
@@ -233,6 +232,12 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
     }
     if (e2 == cudaSuccess) cudaFreeHost(dbg_host);
     if (e2 != cudaSuccess) return e2;
+  }
+  // split-K: partial planes summed in ascending split order, fp32 round-to-nearest
+  if (err == cudaSuccess && pl.splits > 1) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    err = launch_stage2(p.partials, y, p.part_stride, pl.splits, dev, stream);
   }
   return err;
 }

@@ -18,16 +18,17 @@
 // the hf*wf taps re-use each input row; out-of-image positions read as +0.0,
 // the reference's virtual zero padding, tensor.py:112-123) -- TMA cannot do
 // this shift, its tiled boxes need a 16-byte aligned innermost coordinate.
-// Filters arrive by TMA.  Taps are reduced into the same TMEM accumulator,
+// Filters arrive by bulk copy (pre-tiled once per call).  Taps are reduced into the same TMEM accumulator,
 // so the paper's two reductions (channels within a filter row, then across
 // filter rows) both happen inside the tensor core.  Any
 // stride, padding, plane size and channel count are covered.
 //
-// Roles (320 threads, 1 CTA per SM):
-//   warp 0      TMA producer of the filter tiles (one elected lane)
+// Roles (576 threads, 1 CTA per SM):
+//   warp 0      bulk-copy producer of the filter tiles (one elected lane)
 //   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..9  A gather (+ 3xTF32 lo twins of A and of the filter tile),
-//               then the epilogue (tcgen05.ld -> coalesced fp32 stores).
+//   warps 2..17 A gather in two groups taking alternate k-blocks (+ 3xTF32
+//               lo twins of A), then the epilogue (tcgen05.ld -> coalesced
+//               fp32 stores).
 // The tensor core reads an fp32 operand as tf32 by truncation (measured), so
 // the "hi" operands are the raw fp32 tiles and only the lo twins are written.
 // Tile: UMMA M = 128 output pixels = 4 chunks of 32 (a chunk is RC output
@@ -36,13 +37,12 @@
 // UMMA N = NF output channels (16..256), K = 16 input channels per pipeline
 // stage (2 UMMA K-steps of 8).
 //
-// Shared-memory operand layouts (canonical UMMA layouts):
-//   A (pixels, MN-major): chunk i at i*2 KB, [16 c][32 px] rows of 128 B,
-//       128B swizzle with 32-byte atoms (SWIZZLE_128B_BASE32B: the only
-//       MN-major layout tf32 operands support), LBO = 2 KB (next chunk),
-//       SBO = 512 B (next 4 channels)
-//   B (filters, K-major, by TMA): [NF m][16 c] rows of 64 B, SWIZZLE_64B,
-//       SBO = 512 B
+// Shared-memory operand layout (canonical UMMA, both operands K-major, no
+// swizzle): core matrices of 8 rows x 4 channels (128 B), K-adjacent ones
+// 128 B apart (LBO), 8-row groups 512 B apart (SBO).  A (pixels) is written
+// by the loaders with 16-byte stores, B (filters) arrives as one bulk copy
+// of the pre-tiled hi [+ lo] planes per stage.  The 3xTF32 lo planes of the
+// filters are computed once per call by the pre-tiling kernel.
 #pragma once
 
 #include <cuda.h>
@@ -54,11 +54,11 @@ namespace tc {
 
 constexpr int BC = 16;          // input channels per pipeline stage
 constexpr int TILE_P = 128;     // output pixels per tile (UMMA M)
-constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 gather/split + epilogue
+constexpr int THREADS = 576;  // warp 0 bulk copies, warp 1 MMA, warps 2-17 gather + epilogue
 constexpr int A_BYTES = TILE_P * BC * 4;  // 8 KB
 
 struct TcParams {
-  CUtensorMap wmap;  // 3-D (c, m, tap) view of the filters [tap][m][cp]
+  const float *wt;   // filters pre-tiled by filter_tile_kernel: [cb][tap][mtile][plane][NF/8][4][8][4]
   const float *x;    // input [n][c][h][w]
   float *y;
   int C, H, W, HW, S;
@@ -70,13 +70,18 @@ struct TcParams {
   int xblocks;       // chunks per row group: ceil(Wo / xw)
   long long nchunks; // N * rgroups * xblocks
   int PH, PW, WF, taps;
-  int NF, mtiles, cblocks;
+  int NF, mtiles, cblocks, Mp;
+  int splits, kb_per_split;  // split-K over k-blocks (blockIdx.y); partial planes summed by stage2_sum_kernel
+  float *partials;           // [split][n][m][ho][wo] when splits > 1
+  long long part_stride;
   int stages;
   int b_bytes;       // NF * 64
   int stage_bytes;   // (A_BYTES + b_bytes) * (PASSES == 3 ? 2 : 1)
   int tmem_cols;
   uint32_t idesc;    // UMMA instruction descriptor (kind::tf32, M=128, N=NF)
   unsigned long long spin_limit;  // mbarrier wait bound (ns) before __trap: no silent hangs
+  int mode;                       // development only (B2C_TC_MODE): 1 skip gather, 2 skip MMA, 4 skip B split,
+                                  // 8 skip filter copy, 16 skip proxy fence, 32 skip A stores, 128 dumps
   unsigned int *dbg;              // development only (B2C_TC_DEBUG): wait-timeout codes and CTA-0 dumps
 };
 
@@ -124,6 +129,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, unsigne
   }
 }
 
+__device__ __forceinline__ void sts32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ float tf32_lo(float a) { return a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u); }
+
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1, int c2,
                                             int c3) {
   asm volatile(
@@ -131,6 +149,11 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map
       "[%2];" ::"r"(dst),
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,
                                             int c2) {
@@ -143,7 +166,7 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map
 
 // UMMA shared-memory descriptor (sm100 layout: start>>4 [0,14), LBO>>4 [16,30),
 // SBO>>4 [32,46), version 1 [46,48), base offset 0, layout type [61,64)).
-enum : uint64_t { LAYOUT_SW128_BASE32B = 1, LAYOUT_SW128 = 2, LAYOUT_SW64 = 4 };
+enum : uint64_t { LAYOUT_NONE = 0, LAYOUT_SW128_BASE32B = 1, LAYOUT_SW128 = 2, LAYOUT_SW64 = 4 };
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint64_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
@@ -198,18 +221,20 @@ __device__ __forceinline__ Chunk chunk_coords(long long ch, const TcParams &p) {
 
 template <int PASSES>
 __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_constant__ TcParams p) {
-  constexpr int CPT = TILE_P / 32;           // chunks per tile
-  constexpr uint32_t A_LBO = 32 * BC * 4;    // chunk stride: 2 KB
-  constexpr uint32_t A_SBO = 4 * 128;        // 4 channel rows of 128 B
-  constexpr uint32_t A_KSTEP = 8 * 128;      // one UMMA K-step (8 channels)
-  constexpr int LOADERS = THREADS - 64;      // warps 2.. : operand gather/split + epilogue
-  constexpr int CH_PER_LOADER = BC * TILE_P / LOADERS;
+  constexpr int CPT = TILE_P / 32;             // chunks per tile
+  constexpr int LOADERS = THREADS - 64;        // warps 2.. : A gather + epilogue
+  constexpr int GROUPS = 2;                    // loader groups, alternating k-blocks
+  constexpr int GROUP_THREADS = LOADERS / GROUPS;
+  constexpr int CH_PER_LOADER = BC * TILE_P / GROUP_THREADS;  // 8: two 4-channel core-matrix rows
+  constexpr int LA = 2;                        // per-group look-ahead (k-blocks of loads in flight)
+  constexpr uint32_t A_TILE = A_BYTES;         // one A plane (hi or lo)
+  static_assert(CH_PER_LOADER == 8, "loader mapping assumes 8 channels per thread");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = p.stages;
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
-  // bars[0,S): full (filter TMA landed), [S,2S): ready (A gathered + split), [2S,3S): empty (MMA done), [3S]: accum
+  // bars[0,S): full (filter tile landed), [S,2S): ready (A gathered), [2S,3S): empty (MMA done), [3S]: accum
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -218,18 +243,26 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
   const long long pt = blockIdx.x / p.mtiles;
   const int m0 = mt * p.NF;
   const long long ch0 = pt * CPT;
-  const int KB = p.cblocks * p.taps;
+  // split-K: this CTA reduces k-blocks [kb_base, kb_base + KB) of the
+  // (channel block, tap) sequence; kb below is local to the split
+  const int kb_base = blockIdx.y * p.kb_per_split;
+  const int KB = min(p.cblocks * p.taps - kb_base, p.kb_per_split);
   const uint32_t smem_base = smem_u32(smem);
   const uint32_t bar_base = smem_u32(bars);
   auto full_bar = [&](int s) { return bar_base + 8u * s; };
   auto ready_bar = [&](int s) { return bar_base + 8u * (S + s); };
   auto empty_bar = [&](int s) { return bar_base + 8u * (2 * S + s); };
   const uint32_t accum_bar = bar_base + 8u * (3 * S);
+  // stage layout: [A hi | A lo (3xTF32) | B hi | B lo (3xTF32)], every operand in
+  // no-swizzle K-major core matrices (8 rows x 16 B; K-adjacent 128 B apart,
+  // 8-row groups 512 B apart)
+  const uint32_t b_off = A_TILE * (PASSES == 3 ? 2 : 1);
+  const uint32_t b_plane = (uint32_t)p.NF * BC * 4;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
       mbar_init(full_bar(s), 1);
-      mbar_init(ready_bar(s), LOADERS);
+      mbar_init(ready_bar(s), GROUP_THREADS / 32);
       mbar_init(empty_bar(s), 1);
     }
     mbar_init(accum_bar, 1);
@@ -241,7 +274,6 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&p.wmap) : "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -251,60 +283,77 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
 
   if (warp == 0) {
     if (lane == 0) {
-      // ------------------------------------------------ filter-tile TMA producer
+      // ------------------------------------------------ filter-tile bulk-copy producer
+      const bool prof = p.dbg && blockIdx.x == 0;
+      unsigned long long qt_wait = 0;
+      const unsigned long long qt_start = prof ? clock64() : 0;
       for (int kb = 0; kb < KB; kb++) {
         const int s = kb % S;
+        const unsigned long long c0 = prof ? clock64() : 0;
         if (kb >= S) mbar_wait(empty_bar(s), ((kb / S) - 1) & 1, p.spin_limit, p.dbg, 0x100000u | kb);
-        const int cb = kb / p.taps;
-        const int t = kb - cb * p.taps;
+        if (prof) qt_wait += clock64() - c0;
+        if (p.mode & 8) {
+          mbar_arrive(full_bar(s));
+          continue;
+        }
         mbar_expect_tx(full_bar(s), p.b_bytes);
-        tma_load_3d(smem_base + (uint32_t)s * p.stage_bytes + A_BYTES, &p.wmap, full_bar(s), cb * BC, m0, t);
+        // the (cb, tap, filter tile) hi [+ lo] planes are one contiguous pre-tiled block
+        const float *src = p.wt + ((long long)(kb_base + kb) * p.mtiles + mt) * (p.b_bytes / 4);
+        bulk_load(smem_base + (uint32_t)s * p.stage_bytes + b_off, src, p.b_bytes, full_bar(s));
       }
+      if (prof) { p.dbg[5] = (unsigned)qt_wait; p.dbg[6] = (unsigned)(clock64() - qt_start); }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
+      const bool prof = p.dbg && blockIdx.x == 0;
+      unsigned long long mt_wait = 0, mt_issue = 0;
+      const unsigned long long mt_start = prof ? clock64() : 0;
       for (int kb = 0; kb < KB; kb++) {
         const int s = kb % S;
         const uint32_t ph = (kb / S) & 1;
-        if (PASSES == 1) mbar_wait(full_bar(s), ph, p.spin_limit, p.dbg, 0x200000u | kb);
+        unsigned long long c0 = prof ? clock64() : 0;
+        mbar_wait(full_bar(s), ph, p.spin_limit, p.dbg, 0x200000u | kb);
         mbar_wait(ready_bar(s), ph, p.spin_limit, p.dbg, 0x280000u | kb);
         tc_fence_after();
-        if (p.dbg && kb == 0 && blockIdx.x == 0) {  // dump stage 0 of CTA 0
-          const uint32_t *src = reinterpret_cast<const uint32_t *>(smem);
-          for (int i = 0; i < p.stage_bytes / 4 && i < 65536; i++) p.dbg[16 + i] = src[i];
-        }
+        if (prof) { const unsigned long long c = clock64(); mt_wait += c - c0; c0 = c; }
         const uint32_t sa = smem_base + (uint32_t)s * p.stage_bytes;
-        const uint32_t sb = sa + A_BYTES;
-        const uint32_t lo = A_BYTES + p.b_bytes;  // offset of the lo twins
+        const uint32_t sb = sa + b_off;
 #pragma unroll
         for (int k = 0; k < BC / 8; k++) {
-          const uint64_t a_hi = umma_desc(sa + k * A_KSTEP, A_LBO, A_SBO, LAYOUT_SW128_BASE32B);
-          const uint64_t b_hi = umma_desc(sb + k * 32, 16, 512, LAYOUT_SW64);
+          if (p.mode & 2) continue;
+          const uint64_t a_hi = umma_desc(sa + k * 256, 128, 512, LAYOUT_NONE);
+          const uint64_t b_hi = umma_desc(sb + k * 256, 128, 512, LAYOUT_NONE);
           umma_tf32(tmem_d, a_hi, b_hi, p.idesc, (kb | k) != 0);
-          if (PASSES == 3) {
-            const uint64_t a_lo = umma_desc(sa + lo + k * A_KSTEP, A_LBO, A_SBO, LAYOUT_SW128_BASE32B);
-            const uint64_t b_lo = umma_desc(sb + lo + k * 32, 16, 512, LAYOUT_SW64);
-            umma_tf32(tmem_d, a_hi, b_lo, p.idesc, 1);
-            umma_tf32(tmem_d, a_lo, b_hi, p.idesc, 1);
+          if (PASSES == 3) {  // correction terms into their own accumulator (columns NF..2NF):
+            // the main accumulator then sees a third of the accumulation steps
+            const uint64_t a_lo = umma_desc(sa + A_TILE + k * 256, 128, 512, LAYOUT_NONE);
+            const uint64_t b_lo = umma_desc(sb + b_plane + k * 256, 128, 512, LAYOUT_NONE);
+            umma_tf32(tmem_d + p.NF, a_hi, b_lo, p.idesc, (kb | k) != 0);
+            umma_tf32(tmem_d + p.NF, a_lo, b_hi, p.idesc, 1);
           }
         }
         umma_commit(empty_bar(s));  // frees the stage once these MMAs have read it
+        if (prof) mt_issue += clock64() - c0;
       }
       umma_commit(accum_bar);
+      if (prof) { p.dbg[3] = (unsigned)mt_wait; p.dbg[4] = (unsigned)mt_issue; p.dbg[2] = (unsigned)(clock64() - mt_start); }
     }
   } else {
     const int lt = threadIdx.x - 64;  // 0..LOADERS-1
-    // ----------------------------------------------- A-operand gather (+ split)
-    // Loader lt owns tile pixel pix = lt % 128 and CH_PER_LOADER channels of
-    // each 16-channel block.  The shifted input element for tap (ky, kx) is
-    // read straight from global (L1-cached: the 3x3 / 5x5 taps re-touch the
-    // same rows); out-of-image positions read as +0.0 (virtual padding,
-    // tensor.py:112-123).  TMA cannot do this shift: tiled boxes need a
-    // 16-byte aligned innermost coordinate.
-    const int pix = lt & (TILE_P - 1);
-    const int cgrp = lt / TILE_P;
-    long long pbase = -1;  // element offset of (n, 0, iy0, ix0) or -1 for a padding pixel of the tile
+    // ----------------------------------------------------------- A-operand gather
+    // Two loader groups take alternate k-blocks (the per-k-block chain of
+    // barrier waits and shared stores is latency-bound, so the groups overlap).
+    // In a group, thread (pix, cg) owns tile pixel pix and channels 8cg..8cg+7
+    // of each 16-channel block: two 16-byte K-major core-matrix rows.  The
+    // shifted input element for tap (ky, kx) is read straight from global
+    // (L1-cached: the hf*wf taps re-touch the same rows); out-of-image
+    // positions read as +0.0 (virtual padding, tensor.py:112-123).
+    const int grp = lt / GROUP_THREADS;
+    const int gt = lt - grp * GROUP_THREADS;
+    const int pix = gt & (TILE_P - 1);
+    const int cgrp = gt / TILE_P;  // 0 or 1
+    long long pbase = -1;  // element offset of image n, or -1 for a padding pixel of the tile
     int iy0 = 0, ix0 = 0;
     {
       const long long ch = ch0 + (pix >> 5);
@@ -320,63 +369,80 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
         }
       }
     }
-    // smem byte offset of (channel c, pixel pix) in the A tile (32B-atom swizzle)
-    auto a_off = [&](int c) -> uint32_t {
-      const uint32_t L = (uint32_t)((pix >> 5) * 2048 + (c >> 2) * 512 + (c & 3) * 128 + (pix & 31) * 4);
-      return L ^ (((L >> 7) & 3u) << 5);
-    };
+    // shared byte offset of this thread's first core-matrix row; the second
+    // (channels +4) is 128 B further
+    const uint32_t a_row = (uint32_t)((pix >> 3) * 512 + (2 * cgrp) * 128 + (pix & 7) * 16);
     const float *xg = p.x;
-    const int Hh = p.flat ? 1 : p.H;     // flattened 1x1: one "row" of H*W pixels
+    const int Hh = p.flat ? 1 : p.H;  // flattened 1x1: one "row" of H*W pixels
     const int Ww = p.flat ? p.HW : p.W;
-    for (int kb = 0; kb < KB; kb++) {
-      const int s = kb % S;
-      const int cb = kb / p.taps;
-      const int t = kb - cb * p.taps;
+    auto gather = [&](int kb, float (&v)[CH_PER_LOADER]) {
+      const int cb = (kb_base + kb) / p.taps;
+      const int t = (kb_base + kb) - cb * p.taps;
       const int ky = t / p.WF;
       const int kx = t - ky * p.WF;
-      // gather into registers before waiting for the stage to be free
-      float v[CH_PER_LOADER];
       const int c0 = cb * BC + cgrp * CH_PER_LOADER;
       const int iy = iy0 + ky, ix = ix0 + kx;
-      const bool ok = pbase >= 0 && iy >= 0 && iy < Hh && ix >= 0 && ix < Ww;
-      const float *src = xg + pbase + (long long)c0 * p.HW + (long long)iy * Ww + ix;
+      const bool ok = pbase >= 0 && iy >= 0 && iy < Hh && ix >= 0 && ix < Ww && !(p.mode & 1);
+      const float *src = xg + pbase + (long long)c0 * p.HW + iy * Ww + ix;
+      const int nc = ok ? min(CH_PER_LOADER, p.C - c0) : 0;
 #pragma unroll
-      for (int j = 0; j < CH_PER_LOADER; j++) v[j] = (ok && c0 + j < p.C) ? __ldg(src + (long long)j * p.HW) : 0.0f;
-      if (kb >= S) mbar_wait(empty_bar(s), ((kb / S) - 1) & 1, p.spin_limit, p.dbg, 0x300000u | kb);
-      uint8_t *st = smem + (size_t)s * p.stage_bytes;
-      const uint32_t lo = A_BYTES + p.b_bytes;
-#pragma unroll
-      for (int j = 0; j < CH_PER_LOADER; j++) {
-        const uint32_t o = a_off(cgrp * CH_PER_LOADER + j);
-        *reinterpret_cast<float *>(st + o) = v[j];  // the tensor core reads tf32 = v truncated
+      for (int j = 0; j < CH_PER_LOADER; j++) v[j] = j < nc ? __ldg(src + (long long)j * p.HW) : 0.0f;
+    };
+    const bool prof = p.dbg && blockIdx.x == 0 && lt == 0;  // development timing of loader warp 2
+    unsigned long long pt_wait_e = 0, pt_store = 0, pt_fence = 0, pt_gather = 0;
+    auto commit = [&](int kb, const float (&v)[CH_PER_LOADER]) {
+      const int s = kb % S;
+      unsigned long long c0 = prof ? clock64() : 0;
+      if (kb >= S) {  // one lane polls, the warp follows
+        if (lane == 0) mbar_wait(empty_bar(s), ((kb / S) - 1) & 1, p.spin_limit, p.dbg, 0x300000u | kb);
+        __syncwarp();
+      }
+      if (prof) { const unsigned long long c = clock64(); pt_wait_e += c - c0; c0 = c; }
+      const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes + a_row;
+      if (!(p.mode & 32)) {
+        sts128(st, make_float4(v[0], v[1], v[2], v[3]));  // the tensor core reads tf32 = v truncated
+        sts128(st + 128, make_float4(v[4], v[5], v[6], v[7]));
         if (PASSES == 3) {
-          const float h = __uint_as_float(__float_as_uint(v[j]) & 0xFFFFE000u);
-          *reinterpret_cast<float *>(st + lo + o) = v[j] - h;
+          sts128(st + A_TILE, make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3])));
+          sts128(st + A_TILE + 128, make_float4(tf32_lo(v[4]), tf32_lo(v[5]), tf32_lo(v[6]), tf32_lo(v[7])));
         }
       }
-      if (PASSES == 3) {  // filter lo twins once the filter TMA has landed
-        mbar_wait(full_bar(s), (kb / S) & 1, p.spin_limit, p.dbg, 0x380000u | kb);
-        const float4 *b = reinterpret_cast<const float4 *>(st + A_BYTES);
-        float4 *bl = reinterpret_cast<float4 *>(st + lo + A_BYTES);
-        for (int i = lt; i < p.b_bytes / 16; i += LOADERS) {
-          const float4 a = b[i];
-          float4 l;
-          l.x = a.x - __uint_as_float(__float_as_uint(a.x) & 0xFFFFE000u);
-          l.y = a.y - __uint_as_float(__float_as_uint(a.y) & 0xFFFFE000u);
-          l.z = a.z - __uint_as_float(__float_as_uint(a.z) & 0xFFFFE000u);
-          l.w = a.w - __uint_as_float(__float_as_uint(a.w) & 0xFFFFE000u);
-          bl[i] = l;
+      if (prof) { const unsigned long long c = clock64(); pt_store += c - c0; c0 = c; }
+      // generic-proxy smem writes -> visible to the tensor core (async proxy);
+      // one arrival per warp
+      if (!(p.mode & 16)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ready_bar(s));
+      if (prof) pt_fence += clock64() - c0;
+    };
+    // software pipeline over this group's k-blocks: LA of them in flight
+    float v[LA][CH_PER_LOADER];
+    const unsigned long long pt_start = prof ? clock64() : 0;
+#pragma unroll
+    for (int u = 0; u < LA; u++)
+      if (grp + GROUPS * u < KB) gather(grp + GROUPS * u, v[u]);
+    for (int kb0 = grp; kb0 < KB; kb0 += GROUPS * LA) {
+#pragma unroll
+      for (int u = 0; u < LA; u++) {
+        const int kb = kb0 + GROUPS * u;
+        if (kb < KB) {
+          commit(kb, v[u]);
+          const unsigned long long c0 = prof ? clock64() : 0;
+          if (kb + GROUPS * LA < KB) gather(kb + GROUPS * LA, v[u]);
+          if (prof) pt_gather += clock64() - c0;
         }
       }
-      // generic-proxy smem writes -> visible to the tensor core (async proxy)
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(ready_bar(s));
+    }
+    if (prof) {
+      p.dbg[7] = (unsigned)pt_wait_e; p.dbg[8] = (unsigned)pt_store; p.dbg[11] = (unsigned)pt_fence;
+      p.dbg[12] = (unsigned)pt_gather; p.dbg[13] = (unsigned)(clock64() - pt_start);
     }
     // ------------------------------------------------------------------ epilogue
-    mbar_wait(accum_bar, 0, p.spin_limit, p.dbg, 0x400000u);
+    if (lane == 0) mbar_wait(accum_bar, 0, p.spin_limit, p.dbg, 0x400000u);
+    __syncwarp();
     tc_fence_after();
-    const int q = warp & 3;            // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;  // which 32-column groups this warp drains
+    const int q = warp & 3;              // TMEM lane quarter this warp may access
+    const int colgrp = (warp - 2) >> 2;  // which 32-column groups this warp drains
     const int row = q * 32 + lane;
     const int ci = row >> 5;
     const int yi = (row & 31) / p.xw;
@@ -392,16 +458,21 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
       obase = ((long long)c.n * p.M + m0) * p.HoWo + (long long)y * p.Wo + x;
     }
     const int mlim = min(p.NF, p.M - m0);
-    for (int j0 = half * 32; j0 < p.NF; j0 += 64) {
+    constexpr int COLGRPS = LOADERS / 128;
+    for (int j0 = colgrp * 32; j0 < p.NF; j0 += 32 * COLGRPS) {
       uint32_t r[32];
       tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + j0, r);
-      if (p.dbg && blockIdx.x == 0) {  // dump the raw accumulator of CTA 0: [row][col]
-        for (int j = 0; j < 32; j++) p.dbg[16 + 65536 + row * 256 + j0 + j] = r[j];
+      if (PASSES == 3) {  // main + correction accumulator, fp32 round-to-nearest
+        uint32_t c[32];
+        tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + p.NF + j0, c);
+#pragma unroll
+        for (int j = 0; j < 32; j++) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(c[j]));
       }
       if (valid) {
+        float *dst = p.splits > 1 ? p.partials + (long long)blockIdx.y * p.part_stride : p.y;
 #pragma unroll
         for (int j = 0; j < 32; j++)
-          if (j0 + j < mlim) p.y[obase + (long long)(j0 + j) * p.HoWo] = __uint_as_float(r[j]);
+          if (j0 + j < mlim) dst[obase + (long long)(j0 + j) * p.HoWo] = __uint_as_float(r[j]);
       }
     }
   }
@@ -413,18 +484,36 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
   }
 }
 
-// Filters [m][c][ky][kx] -> [tap][m][cp] (cp = C rounded up to 4, zero padded):
-// the K-major layout TMA needs (16-byte row strides).  Weight-only (no input
-// data is transformed), one launch per call, 4*taps*M*cp bytes of workspace.
-__global__ void __launch_bounds__(256) filter_relayout_kernel(const float *__restrict__ w, float *__restrict__ wp,
-                                                              int M, int C, int Cp, int taps) {
-  const long long total = (long long)taps * M * Cp;
+// Filters [m][c][ky][kx] -> pre-tiled [cb][tap][filter tile][plane][NF/8][4][8][4]:
+// for every 16-channel block cb, tap and filter tile, the NF x 16 operand in
+// the UMMA no-swizzle K-major core-matrix order (8 rows x 16 bytes per core
+// matrix; K-adjacent core matrices 128 B apart, 8-row groups 512 B apart),
+// zero padded beyond M and C.  planes = 2 (3xTF32) appends the lo plane
+// w - tf32(w).  Every pipeline stage's filter operands are then ONE
+// contiguous block moved by a single bulk copy.  Weight-only (no input data
+// is transformed): one launch per call.
+__global__ void __launch_bounds__(256) filter_tile_kernel(const float *__restrict__ w, float *__restrict__ wt, int M,
+                                                          int C, int taps, int NF, int mtiles, int cblocks,
+                                                          int planes) {
+  const long long tile = (long long)NF * BC;
+  const long long total = (long long)cblocks * taps * mtiles * planes * tile;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(i % Cp);
-    const long long r = i / Cp;
-    const int m = (int)(r % M);
-    const int t = (int)(r / M);
-    wp[i] = c < C ? w[((long long)m * C + c) * taps + t] : 0.0f;
+    const int within = (int)(i % tile);
+    const long long blk = i / tile;
+    const int plane = (int)(blk % planes);
+    const long long kbm = blk / planes;  // (cb, tap, filter tile)
+    const int mt = (int)(kbm % mtiles);
+    const long long kb = kbm / mtiles;
+    const int t = (int)(kb % taps);
+    const int cb = (int)(kb / taps);
+    const int e = within & 3;         // element within a 16-byte core-matrix row
+    const int r = (within >> 2) & 7;  // row within the core matrix
+    const int j = (within >> 5) & 3;  // core matrix along K (4 channels each)
+    const int g = within >> 7;        // 8-row group
+    const int m = mt * NF + g * 8 + r;
+    const int c = cb * BC + j * 4 + e;
+    const float v = (m < M && c < C) ? w[((long long)m * C + c) * taps + t] : 0.0f;
+    wt[i] = plane == 0 ? v : tf32_lo(v);
   }
 }
 

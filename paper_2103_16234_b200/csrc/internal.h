@@ -36,14 +36,15 @@ struct TcPlan {
   int passes = 3;    // 3: 3xTF32 (fp32-class), 1: TF32
   bool flat = false; // 1x1: pixels flattened over the plane
   long long nchunks = 0;
-  long long grid = 0;
+  long long grid = 0;  // CTAs incl. splits
+  int splits = 1, kb_per_split = 0;  // split-K over (channel block, tap) k-blocks
   double cost = 0;
 };
 bool tc_supported(const Geom &g);
 bool tc_flat(const Geom &g);
-bool tc_needs_relayout(const Geom &g, const float *w);
-long long tc_workspace_bytes(const Geom &g);
-bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, TcPlan *out);
+long long tc_workspace_bytes(const Geom &g, const TcPlan &pl);
+bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced_splits, TcPlan *out);
+long long tc_filter_bytes(const Geom &g, const TcPlan &pl);
 cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const float *w, float *y, void *workspace,
                       long long ws_bytes, cudaStream_t stream);
 

@@ -74,6 +74,7 @@ class ConvLayer:
         if self.tensor_core:
             self._tc = nat.TcPlanC()
             self._tc.filters_per_tile = int(filters_per_tile)
+            self._tc.splits = int(splits)
             nat.check(self._lib.b2c_tc_select_tiles(ctypes.byref(self._desc), self._engine_id, ctypes.byref(self._tc)))
         else:
             e = nat.ENGINE_TWOSTAGE if engine == "twostage" else nat.ENGINE_FUSED
@@ -92,7 +93,8 @@ class ConvLayer:
     def family(self) -> str:
         if self.tensor_core:
             t = self._tc
-            return f"{self.engine}_x{t.pixels_per_chunk}_n{t.filters_per_tile}_s{t.stages}" + ("_flat" if t.flattened else "")
+            return (f"{self.engine}_x{t.pixels_per_chunk}_n{t.filters_per_tile}_s{t.stages}_k{t.splits}"
+                    + ("_flat" if t.flattened else ""))
         return self._lib.b2c_family_name(self._tiles.family).decode()
 
     @property
@@ -101,7 +103,7 @@ class ConvLayer:
 
     @property
     def splits(self) -> int:
-        return int(self._tiles.splits)
+        return int(self._tc.splits if self.tensor_core else self._tiles.splits)
 
     def output_shape(self) -> tuple[int, int, int, int]:
         return (self.cfg.n, self.cfg.m, *self.out_hw)
@@ -126,7 +128,8 @@ class ConvLayer:
                 self._ws = torch.empty(self.workspace_bytes // 4, dtype=torch.float32, device=x.device)
             ws_ptr = self._ws.data_ptr() if self.workspace_bytes else None
             st = self._lib.b2c_conv2d_forward_tc(ctypes.byref(self._desc), x.data_ptr(), w.data_ptr(), out.data_ptr(),
-                                                 ws_ptr, self.workspace_bytes, self._engine_id, ctypes.c_void_p(s))
+                                                 ws_ptr, self.workspace_bytes, self._engine_id, ctypes.byref(self._tc),
+                                                 ctypes.c_void_p(s))
             nat.check(st)
         else:
             if self.workspace_bytes and (self._ws is None or self._ws.device != x.device):

@@ -270,3 +270,73 @@ def test_tile_planner_forced_family_and_split(native):
     assert t.splits == 4
     with pytest.raises(pk.InvalidPlan):
         pk.select_tiles(cfg, family=names.index("fused_1x1s1_m32"))
+
+
+# --- the tensor-core (tcgen05) planner ------------------------------------------
+
+def _tc_plan(native, cfg, engine, nf=0):
+    import ctypes
+
+    from paper_2103_16234_b200 import _native as nat
+
+    plan = nat.TcPlanC()
+    plan.filters_per_tile = nf
+    st = native.b2c_tc_select_tiles(ctypes.byref(nat.desc(cfg)), nat.ENGINES[engine], ctypes.byref(plan))
+    nat.check(st)
+    return plan
+
+
+def test_tensor_core_planner_covers_every_baseline_layer(native):
+    from paper_2103_16234_b200 import workloads as W
+
+    for wl, (_, batches) in W.WORKLOADS.items():
+        for n in batches:
+            for cfg in W.layers(wl, n):
+                ho, wo = pk.output_dims(cfg)
+                for engine in ("tf32x3", "tf32"):
+                    p = _tc_plan(native, cfg, engine)
+                    assert p.passes == (3 if engine == "tf32x3" else 1)
+                    assert p.pixels_per_chunk in (8, 16, 32) and p.filters_per_tile % 16 == 0
+                    assert 16 <= p.filters_per_tile <= 256 and p.filter_tiles * p.filters_per_tile >= cfg.m
+                    assert p.stages >= 2 and p.smem_bytes <= 227 * 1024
+                    cols = p.filters_per_tile * (2 if engine == "tf32x3" else 1)
+                    assert cols <= p.tmem_columns <= 512 and p.tmem_columns & (p.tmem_columns - 1) == 0
+                    flat = cfg.hf == cfg.wf == 1 and cfg.stride == 1 and cfg.pad_h == cfg.pad_w == 0
+                    assert bool(p.flattened) == flat
+                    width = ho * wo if flat else wo
+                    rows = 1 if flat else ho
+                    xw = p.pixels_per_chunk
+                    chunks = cfg.n * -(-rows // (32 // xw)) * -(-width // xw)
+                    assert p.grid == -(-chunks // 4) * p.filter_tiles * p.splits, (wl, cfg.name)
+                    planes = 2 if engine == "tf32x3" else 1
+                    kb = -(-cfg.c // 16) * cfg.hf * cfg.wf
+                    assert 1 <= p.splits <= kb
+                    if engine == "tf32x3":
+                        assert -(-kb // p.splits) <= 72  # <= 1152 products per split (accuracy rule)
+                    filt = 4 * kb * 16 * p.filter_tiles * p.filters_per_tile * planes
+                    part = 4 * p.splits * cfg.n * cfg.m * ho * wo if p.splits > 1 else 0
+                    assert p.workspace_bytes == -(-filt // 256) * 256 + part
+
+
+def test_tensor_core_planner_forced_tiles_and_errors(native):
+    import ctypes
+
+    from paper_2103_16234_b200 import _native as nat
+
+    cfg = pk.ConvConfig("t", n=2, c=40, h=12, w=12, m=96, hf=3, wf=3, pad_h=1, pad_w=1)
+    for nf in (16, 32, 48, 96, 256):
+        p = _tc_plan(native, cfg, "tf32x3", nf)
+        assert p.filters_per_tile == nf and p.filter_tiles == -(-96 // nf)
+    for bad in (8, 24, 272):
+        with pytest.raises(pk.InvalidPlan):
+            _tc_plan(native, cfg, "tf32", bad)
+    plan = nat.TcPlanC()
+    assert native.b2c_tc_select_tiles(ctypes.byref(nat.desc(cfg)), nat.ENGINE_FUSED, ctypes.byref(plan)) \
+        == nat.INVALID_ARGUMENT
+    # device compute entry validates before touching the GPU
+    assert native.b2c_conv2d_forward_tc(ctypes.byref(nat.desc(cfg)), None, None, None, None, 0, nat.ENGINE_TF32X3,
+                                        None, None) == nat.INVALID_ARGUMENT
+    p = nat.TcPlanC()
+    p.splits = 3
+    assert native.b2c_tc_select_tiles(ctypes.byref(nat.desc(cfg)), nat.ENGINE_TF32, ctypes.byref(p)) == nat.OK
+    assert p.splits == 3

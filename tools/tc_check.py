@@ -97,6 +97,12 @@ CASES = {
 
 if __name__ == "__main__":
     import subprocess
+    if len(sys.argv) > 2 and sys.argv[1] == "time":  # time WL N name,name,...
+        torch.cuda.set_device(0)
+        for spec in sys.argv[2:]:
+            wl, n, names = spec.split(":")
+            timing(wl, int(n), names=set(names.split(",")) if names else None)
+        sys.exit(0)
     if len(sys.argv) > 2 and sys.argv[1] == "case":
         torch.cuda.set_device(0)
         case(sys.argv[2], *CASES[sys.argv[2]])
