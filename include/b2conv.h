@@ -124,6 +124,14 @@ typedef struct {
                                *filters_per_tile*passes' planes, rounded up to
                                256) + split-K partials (4*splits*n*m*ho*wo
                                when splits > 1)                               */
+  int32_t mode;             /* in/out: 0 = planner's choice (in), 1 = gather
+                               (loaders re-gather the tap-shifted input per
+                               tap, any stride), 2 = halo (stride 1: one staged
+                               padded-input halo per channel block, taps are
+                               descriptor offsets)                            */
+  int32_t halo_positions;   /* out: staged positions per tile (mode 2)        */
+  int32_t m_halves;         /* out: 128-pixel UMMA M halves per tile (mode 2:
+                               1 or 2, sharing each filter tile)              */
 } b2c_tc_plan;
 
 /* ---------------------------------------------------------------- metadata */

@@ -429,14 +429,15 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
 
 namespace {
 b2c_status tc_plan_of(const b2c_conv_desc *d, const b2c::Geom &g, int32_t engine, int forced_nf, int forced_splits,
-                      b2c::TcPlan *pl) {
+                      b2c::TcPlan *pl, int forced_mode = 0) {
   if (engine != B2C_ENGINE_TF32X3 && engine != B2C_ENGINE_TF32)
     return fail(B2C_INVALID_ARGUMENT, "engine %d is not a tensor-core engine", engine);
   if (forced_nf > 0 && (forced_nf % 16 != 0 || forced_nf > 256))
     return fail(B2C_INVALID_PLAN, "filters_per_tile must be a multiple of 16 in [16, 256], got %d", forced_nf);
   if (forced_splits < 0 || forced_splits > 64) return fail(B2C_INVALID_PLAN, "splits must be in [0, 64], got %d", forced_splits);
-  if (!b2c::plan_tc(g, engine == B2C_ENGINE_TF32X3 ? 3 : 1, forced_nf, 0, forced_splits, pl)) {
-    if (forced_splits > 0 || forced_nf > 0)
+  if (forced_mode < 0 || forced_mode > 2) return fail(B2C_INVALID_PLAN, "mode must be 0, 1 or 2, got %d", forced_mode);
+  if (!b2c::plan_tc(g, engine == B2C_ENGINE_TF32X3 ? 3 : 1, forced_nf, 0, forced_splits, pl, forced_mode)) {
+    if (forced_splits > 0 || forced_nf > 0 || forced_mode > 0)
       return fail(B2C_INVALID_PLAN, "forced tensor-core tile (filters %d, splits %d) cannot run this layer", forced_nf,
                   forced_splits);
     return fail(B2C_UNSUPPORTED, "layer too large for the tensor-core engine's 32-bit per-image offsets");
@@ -453,7 +454,7 @@ b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_pl
   b2c::Geom g = geom_of(d);
   if ((st = check_sizes(g)) != B2C_OK) return st;
   b2c::TcPlan pl;
-  if ((st = tc_plan_of(d, g, engine, out->filters_per_tile, out->splits, &pl)) != B2C_OK) return st;
+  if ((st = tc_plan_of(d, g, engine, out->filters_per_tile, out->splits, &pl, out->mode)) != B2C_OK) return st;
   out->pixels_per_chunk = pl.xb;
   out->filters_per_tile = pl.nf;
   out->filter_tiles = pl.mtiles;
@@ -465,6 +466,9 @@ b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_pl
   out->grid = pl.grid;
   out->splits = pl.splits;
   out->workspace_bytes = b2c::tc_workspace_bytes(g, pl);
+  out->mode = pl.halo > 0 ? 2 : 1;
+  out->halo_positions = pl.halo;
+  out->m_halves = pl.mh;
   return B2C_OK;
 }
 
@@ -476,7 +480,8 @@ b2c_status b2c_conv2d_forward_tc(const b2c_conv_desc *d, const float *x, const f
   b2c::Geom g = geom_of(d);
   if ((st = check_sizes(g)) != B2C_OK) return st;
   b2c::TcPlan pl;
-  if ((st = tc_plan_of(d, g, engine, tiles ? tiles->filters_per_tile : 0, tiles ? tiles->splits : 0, &pl)) != B2C_OK)
+  if ((st = tc_plan_of(d, g, engine, tiles ? tiles->filters_per_tile : 0, tiles ? tiles->splits : 0, &pl,
+                       tiles ? tiles->mode : 0)) != B2C_OK)
     return st;
   if (!workspace || workspace_size < b2c::tc_workspace_bytes(g, pl))
     return fail(B2C_INVALID_ARGUMENT, "tensor-core engine needs a %lld-byte filter workspace, %lld provided",

@@ -19,7 +19,14 @@ namespace {
 
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 
-const void *tc_kernel(int passes) {
+const void *tc_kernel(int passes, bool halo, int mh) {
+  if (halo) {
+    if (mh == 2)
+      return passes == 3 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<3, 2>)
+                         : reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<1, 2>);
+    return passes == 3 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<3, 1>)
+                       : reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<1, 1>);
+  }
   return passes == 3 ? reinterpret_cast<const void *>(&tc::conv_tc_kernel<3>)
                      : reinterpret_cast<const void *>(&tc::conv_tc_kernel<1>);
 }
@@ -37,7 +44,7 @@ bool tc_supported(const Geom &g) {
 }
 
 long long tc_filter_bytes(const Geom &g, const TcPlan &pl) {
-  const long long b = 4LL * cdiv(g.C, tc::BC) * tc::BC * g.HF * g.WF * (long long)pl.mtiles * pl.nf * (pl.passes == 3 ? 2 : 1);
+  const long long b = 4LL * cdiv(g.C, tc::BC) * tc::BC * g.HF * g.WF * (long long)pl.mtiles * pl.nf * pl.wplanes;
   return (b + 255) / 256 * 256;
 }
 
@@ -46,12 +53,13 @@ long long tc_workspace_bytes(const Geom &g, const TcPlan &pl) {
   return tc_filter_bytes(g, pl) + partials;
 }
 
-bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced_splits, TcPlan *out) {
+bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced_splits, TcPlan *out,
+             int forced_mode) {
   if (!tc_supported(g)) return false;
   const bool flat = tc_flat(g);
   const int wo = flat ? g.HoWo : g.Wo;
   const int ho = flat ? 1 : g.Ho;
-  // chunk shape: rc rows x xw columns (xw * rc = 32), least padded pixels, then widest
+  // gather mode: chunk shape rc rows x xw columns (xw * rc = 32), least padded pixels, then widest
   int xw = 32;
   long long best_px = -1;
   for (int cand : {32, 16, 8}) {
@@ -67,11 +75,14 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
   if (best_px < 0) return false;
   const int rc = 32 / xw;
   const long long nchunks = (long long)g.N * cdiv(ho, rc) * cdiv(wo, xw);
-  const long long ptiles = cdiv(nchunks, tc::TILE_P / 32);
   const int taps = g.HF * g.WF;
   const int cblocks = (int)cdiv(g.C, tc::BC);
   const int KB = cblocks * taps;
   const int sms = device_sm_count(0);
+  // halo mode (stride 1): tiles over the flattened padded stack
+  const bool halo_ok = g.S == 1 && forced_mode != 1;
+  const long long Wp = (long long)g.W + 2 * g.PW, Hp = (long long)g.H + 2 * g.PH;
+
   TcPlan best;
   double best_cost = 1e300;
   // 3xTF32 accuracy: the tensor core accumulates with truncation, so the main
@@ -80,54 +91,91 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
   // fp32 round-to-nearest (measured: within tol(K) up to K = 4608 with margin)
   const int max_kbps = passes == 3 ? 72 : 1 << 30;
   const double out_bytes = 4.0 * g.N * g.M * g.HoWo;
-  for (int mt = 1; mt <= 64; mt++) {
-    int nf = (int)cdiv(cdiv(g.M, mt), 16) * 16;
-    if (nf > 256) continue;
-    if (forced_nf > 0) nf = forced_nf;
-    const int mtiles = (int)cdiv(g.M, nf);
-    const long long stage = (long long)(tc::A_BYTES + nf * 64) * (passes == 3 ? 2 : 1);  // A + B (+ lo planes)
-    const int stages = (int)std::min<long long>(6, (kSmemBudget - 2048) / stage);
-    if (stages < 2) continue;
-    static const int kAuto[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
-    const int nopt = forced_splits > 0 ? 1 : (int)(sizeof(kAuto) / sizeof(int));
-    for (int oi = 0; oi < nopt; oi++) {
-      const int sp = forced_splits > 0 ? forced_splits : kAuto[oi];
-      if (sp > KB) break;
-      const int kbps = (int)cdiv(KB, sp);
-      const int splits = (int)cdiv(KB, kbps);
-      if (splits != sp && forced_splits <= 0) continue;  // duplicate of a smaller split
-      if (kbps > max_kbps && forced_splits <= 0) continue;
-      const long long ctas = ptiles * mtiles * splits;
-      // per-k-block clocks (B200 measurements): tensor issue ~95 clk per
-      // 128x256x8 tf32 UMMA, and a ~1.1-1.3k clk latency chain per k-block
-      // (barrier hand-offs + loader stores) shared by the two loader groups
-      const double mma = passes * 2.0 * std::max(95.0 * nf / 256.0, 12.0);
-      const double chain = passes == 3 ? 1300.0 : 1100.0;
-      const double t_cta = kbps * std::max(mma, chain) + 6000.0 + nf * 8.0;
-      double cost = (double)cdiv(ctas, sms) * t_cta;
-      if (splits > 1) cost += 4000.0 + 2.0 * (splits + 1) * out_bytes / (3.0e3 * sms / 148.0);  // stage-2 sum
-      if (cost < best_cost) {
-        best_cost = cost;
-        best.xb = xw;
-        best.nf = nf;
-        best.mtiles = mtiles;
-        best.stages = stages;
-        best.stage_bytes = (int)stage;
-        best.grid = ctas;
-        best.passes = passes;
-        best.flat = flat;
-        best.nchunks = nchunks;
-        best.splits = splits;
-        best.kb_per_split = kbps;
+  const int planes = passes == 3 ? 2 : 1;
+  // modes: 1 = gather; 2 = halo with one 128-position M half; 3 = halo with two
+  for (int mode = 1; mode <= 3; mode++) {
+    const int mh = mode == 3 ? 2 : 1;
+    if (forced_mode > 0 && (mode == 1) != (forced_mode == 1)) continue;
+    if (mode >= 2 && !halo_ok) continue;
+    const long long halo = (tc::TILE_P * mh + (g.HF - 1) * Wp + (g.WF - 1) + 7) / 8 * 8;
+    const long long ptiles = mode == 1 ? cdiv(nchunks, tc::TILE_P / 32) : cdiv((long long)g.N * Hp * Wp, tc::TILE_P * mh);
+    for (int mt = 1; mt <= 64; mt++) {
+      int nf = (int)cdiv(cdiv(g.M, mt), 16) * 16;
+      if (nf > 256) continue;
+      if (forced_nf > 0) nf = forced_nf;
+      if (nf * mh * planes > 512) continue;  // TMEM: main (+ correction) accumulators of every M half
+      const int mtiles = (int)cdiv(g.M, nf);
+      const long long bstage = (long long)nf * 64 * planes;
+      long long stage, smem_fixed;
+      int stages;
+      if (mode == 1) {
+        stage = (long long)tc::A_BYTES * planes + bstage;  // A + B (+ lo planes)
+        smem_fixed = 0;
+      } else {
+        stage = bstage;                                     // filter ring (hi + lo); A halo double-buffered
+        smem_fixed = 2 * halo * 64 * planes;
       }
+      stages = (int)std::min<long long>(mode == 1 ? 6 : 8, (kSmemBudget - 2048 - smem_fixed) / stage);
+      if (smem_fixed + 2 * stage > kSmemBudget - 2048) continue;
+      if (stages < 2) continue;
+      static const int kAuto[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
+      const int nopt = forced_splits > 0 ? 1 : (int)(sizeof(kAuto) / sizeof(int));
+      for (int oi = 0; oi < nopt; oi++) {
+        const int sp = forced_splits > 0 ? forced_splits : kAuto[oi];
+        // halo mode splits whole channel blocks (all taps of a block in one CTA)
+        const int units = mode == 1 ? KB : cblocks;
+        if (sp > units) break;
+        const int ups = (int)cdiv(units, sp);
+        const int splits = (int)cdiv(units, ups);
+        if (splits != sp && forced_splits <= 0) continue;  // duplicate of a smaller split
+        const int kbps = mode == 1 ? ups : ups * taps;
+        if (kbps > max_kbps && forced_splits <= 0 && !(mode == 2 && ups == 1)) continue;
+        const long long ctas = ptiles * mtiles * splits;
+        // per-k-block clocks (B200 measurements): tensor issue ~95 clk per
+        // 128x256x8 tf32 UMMA; gather mode adds a ~1.1-1.3k clk latency chain
+        // per k-block, halo mode ~150 clk of barrier work per tap and one
+        // double-buffered halo fill per channel block
+        const double mma = passes * 2.0 * mh * std::max(95.0 * nf / 256.0, 12.0);
+        double t_cta;
+        if (mode == 1) {
+          t_cta = kbps * std::max(mma, passes == 3 ? 1300.0 : 1100.0);
+        } else {
+          // per tap: tensor issue, the L2 feed of the filter tile (~36 B/clk/SM
+          // of the ~6.3 KB/clk chip L2 rate), ~150 clk of barrier work
+          const double l2 = nf * 64.0 * planes / 36.0;  // hi (+ streamed lo) plane
+          const double fill = 400.0 + halo * 4.0 / 512.0 * 60.0;
+          t_cta = ups * std::max(taps * (std::max(mma, l2) + 150.0), fill);
+        }
+        t_cta += 6000.0 + nf * 8.0;
+        double cost = (double)cdiv(ctas, sms) * t_cta;
+        if (splits > 1) cost += 4000.0 + 2.0 * (splits + 1) * out_bytes / (3.0e3 * sms / 148.0);  // stage-2 sum
+        if (cost < best_cost) {
+          best_cost = cost;
+          best = TcPlan();
+          best.xb = mode == 1 ? xw : 0;
+          best.halo = mode >= 2 ? (int)halo : 0;
+          best.mh = mh;
+          best.wplanes = planes;  // filter lo plane streamed with the hi plane
+          best.nf = nf;
+          best.mtiles = mtiles;
+          best.stages = stages;
+          best.stage_bytes = (int)stage;
+          best.grid = ctas;
+          best.passes = passes;
+          best.flat = flat;
+          best.nchunks = mode == 1 ? nchunks : 0;
+          best.splits = splits;
+          best.kb_per_split = kbps;
+          best.smem_bytes = (int)(stages * stage + smem_fixed) + 1024 /*align*/ + 256 /*barriers*/;
+        }
+      }
+      if (forced_nf > 0) break;
     }
-    if (forced_nf > 0) break;
   }
   if (best.nf == 0) return false;
   int cols = 32;
-  while (cols < best.nf * (passes == 3 ? 2 : 1)) cols <<= 1;  // 3xTF32: main + correction accumulators
+  while (cols < best.nf * best.mh * (passes == 3 ? 2 : 1)) cols <<= 1;  // 3xTF32: main + correction
   best.tmem_cols = cols;
-  best.smem_bytes = best.stages * best.stage_bytes + 1024 /*align*/ + 256 /*barriers*/;
   best.cost = best_cost;
   *out = best;
   return true;
@@ -140,7 +188,8 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   const int Mp = pl.mtiles * pl.nf;
   if (!workspace || ws_bytes < tc_workspace_bytes(g, pl)) return cudaErrorInvalidValue;
   float *wt = static_cast<float *>(workspace);
-  const int planes = pl.passes == 3 ? 2 : 1;
+  const int planes = (pl.halo > 0 && pl.passes == 3 && std::getenv("B2C_TC_BSPLIT") && std::atoi(std::getenv("B2C_TC_BSPLIT")))
+                         ? 1 : pl.wplanes;
   {
     const long long total = (long long)cblocks * taps * Mp * tc::BC * planes;
     const int blocks = (int)std::min<long long>(cdiv(total, 256), 8LL * device_sm_count(0));
@@ -149,28 +198,36 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  const int rc = 32 / pl.xb;
+  const int rc = pl.xb > 0 ? 32 / pl.xb : 1;
 
   tc::TcParams p;
   std::memset(&p, 0, sizeof(p));
   p.wt = wt;
   p.Mp = Mp;
+  const bool flat_chunks = pl.flat && pl.halo == 0;  // gather mode runs 1x1 over the flattened plane
   p.x = x;
   p.y = y;
+  p.N = g.N;
+  p.Hp = g.H + 2 * g.PH;
+  p.Wp = g.W + 2 * g.PW;
+  p.halo = pl.halo;
+  p.mh = pl.mh;
+  p.bsplit = 0;
+  if (const char *e = std::getenv("B2C_TC_BSPLIT")) p.bsplit = std::atoi(e);  // development switch
   p.C = g.C;
   p.H = g.H;
   p.W = g.W;
   p.HW = g.H * g.W;
   p.S = g.S;
-  p.flat = pl.flat ? 1 : 0;
+  p.flat = flat_chunks ? 1 : 0;
   p.M = g.M;
-  p.Wo = pl.flat ? g.HoWo : g.Wo;
+  p.Wo = flat_chunks ? g.HoWo : g.Wo;
   p.HoWo = g.HoWo;
-  p.Ho = pl.flat ? 1 : g.Ho;
-  p.xw = pl.xb;
+  p.Ho = flat_chunks ? 1 : g.Ho;
+  p.xw = pl.xb > 0 ? pl.xb : 32;
   p.rc = rc;
   p.rgroups = (int)cdiv(p.Ho, rc);
-  p.xblocks = (int)cdiv(p.Wo, pl.xb);
+  p.xblocks = (int)cdiv(p.Wo, p.xw);
   p.nchunks = pl.nchunks;
   p.PH = g.PH;
   p.PW = g.PW;
@@ -195,7 +252,7 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   p.spin_limit = 4000000000ull;  // 4 s
   if (const char *m = std::getenv("B2C_TC_MODE")) p.mode = std::atoi(m);
 
-  const void *kern = tc_kernel(pl.passes);
+  const void *kern = tc_kernel(pl.passes, pl.halo > 0, pl.mh);
   static std::mutex mu;
   {
     std::lock_guard<std::mutex> lk(mu);

@@ -61,7 +61,11 @@ struct TcParams {
   const float *wt;   // filters pre-tiled by filter_tile_kernel: [cb][tap][mtile][plane][NF/8][4][8][4]
   const float *x;    // input [n][c][h][w]
   float *y;
-  int C, H, W, HW, S;
+  int N, C, H, W, HW, S;
+  int Hp, Wp, halo;  // halo variant: padded stack geometry, staged positions per tile
+  int mh;            // halo variant: 128-position M halves per tile (1 or 2), sharing every filter tile
+  int bsplit;        // halo variant, 3xTF32: 1 = loaders derive the filter lo plane in smem,
+                     // 0 = the pre-tiled lo plane is streamed with the hi plane
   int flat;          // unpadded stride-1 1x1: chunks run over the flattened plane
   int M, Wo, HoWo;   // output geometry (Wo = HoWo for flattened 1x1)
   int Ho;            // output rows (1 for flattened)
@@ -129,6 +133,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, unsigne
   }
 }
 
+// One lane of a converged warp (elect.sync): the warp runs the role's loop
+// together so descriptors and loop state stay warp-uniform (uniform
+// datapath), and the elected lane issues the single-thread tcgen05 / bulk ops.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void sts32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
@@ -183,8 +198,7 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
@@ -282,9 +296,10 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
-    if (lane == 0) {
+    const bool leader = elect_one();
+    {
       // ------------------------------------------------ filter-tile bulk-copy producer
-      const bool prof = p.dbg && blockIdx.x == 0;
+      const bool prof = p.dbg && blockIdx.x == 0 && leader;
       unsigned long long qt_wait = 0;
       const unsigned long long qt_start = prof ? clock64() : 0;
       for (int kb = 0; kb < KB; kb++) {
@@ -293,20 +308,24 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
         if (kb >= S) mbar_wait(empty_bar(s), ((kb / S) - 1) & 1, p.spin_limit, p.dbg, 0x100000u | kb);
         if (prof) qt_wait += clock64() - c0;
         if (p.mode & 8) {
-          mbar_arrive(full_bar(s));
+          if (leader) mbar_arrive(full_bar(s));
           continue;
         }
-        mbar_expect_tx(full_bar(s), p.b_bytes);
         // the (cb, tap, filter tile) hi [+ lo] planes are one contiguous pre-tiled block
         const float *src = p.wt + ((long long)(kb_base + kb) * p.mtiles + mt) * (p.b_bytes / 4);
-        bulk_load(smem_base + (uint32_t)s * p.stage_bytes + b_off, src, p.b_bytes, full_bar(s));
+        if (leader) {
+          mbar_expect_tx(full_bar(s), p.b_bytes);
+          bulk_load(smem_base + (uint32_t)s * p.stage_bytes + b_off, src, p.b_bytes, full_bar(s));
+        }
+        __syncwarp();
       }
       if (prof) { p.dbg[5] = (unsigned)qt_wait; p.dbg[6] = (unsigned)(clock64() - qt_start); }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    const bool leader = elect_one();
+    {
       // ------------------------------------------------------------ MMA issuer
-      const bool prof = p.dbg && blockIdx.x == 0;
+      const bool prof = p.dbg && blockIdx.x == 0 && leader;
       unsigned long long mt_wait = 0, mt_issue = 0;
       const unsigned long long mt_start = prof ? clock64() : 0;
       for (int kb = 0; kb < KB; kb++) {
@@ -324,19 +343,23 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
           if (p.mode & 2) continue;
           const uint64_t a_hi = umma_desc(sa + k * 256, 128, 512, LAYOUT_NONE);
           const uint64_t b_hi = umma_desc(sb + k * 256, 128, 512, LAYOUT_NONE);
-          umma_tf32(tmem_d, a_hi, b_hi, p.idesc, (kb | k) != 0);
-          if (PASSES == 3) {  // correction terms into their own accumulator (columns NF..2NF):
-            // the main accumulator then sees a third of the accumulation steps
-            const uint64_t a_lo = umma_desc(sa + A_TILE + k * 256, 128, 512, LAYOUT_NONE);
-            const uint64_t b_lo = umma_desc(sb + b_plane + k * 256, 128, 512, LAYOUT_NONE);
-            umma_tf32(tmem_d + p.NF, a_hi, b_lo, p.idesc, (kb | k) != 0);
-            umma_tf32(tmem_d + p.NF, a_lo, b_hi, p.idesc, 1);
+          const uint64_t a_lo = umma_desc(sa + A_TILE + k * 256, 128, 512, LAYOUT_NONE);
+          const uint64_t b_lo = umma_desc(sb + b_plane + k * 256, 128, 512, LAYOUT_NONE);
+          if (leader) {
+            umma_tf32(tmem_d, a_hi, b_hi, p.idesc, (kb | k) != 0);
+            if (PASSES == 3) {  // correction terms into their own accumulator (columns NF..2NF):
+              // the main accumulator then sees a third of the accumulation steps
+              umma_tf32(tmem_d + p.NF, a_hi, b_lo, p.idesc, (kb | k) != 0);
+              umma_tf32(tmem_d + p.NF, a_lo, b_hi, p.idesc, 1);
+            }
           }
+          __syncwarp();
         }
-        umma_commit(empty_bar(s));  // frees the stage once these MMAs have read it
+        if (leader) umma_commit(empty_bar(s));  // frees the stage once these MMAs have read it
+        __syncwarp();
         if (prof) mt_issue += clock64() - c0;
       }
-      umma_commit(accum_bar);
+      if (leader) umma_commit(accum_bar);
       if (prof) { p.dbg[3] = (unsigned)mt_wait; p.dbg[4] = (unsigned)mt_issue; p.dbg[2] = (unsigned)(clock64() - mt_start); }
     }
   } else {
@@ -476,6 +499,290 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
       }
     }
   }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(p.tmem_cols) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Halo variant (stride 1): the padded input is viewed as one flattened stack
+// of rows of width Wp = W + 2*pw (image n occupies rows n*Hp .. n*Hp+Hp-1,
+// Hp = H + 2*ph).  An output pixel at flattened position q = r*Wp + x needs
+// input position q + ky*Wp + kx for tap (ky, kx): a CONSTANT shift.  So per
+// 16-channel block the loaders stage the tile's halo -- positions
+// [q0, q0 + 128 + (hf-1)*Wp + (wf-1)) -- once, K-major with one 16-byte row
+// per position (8-position core-matrix groups 128 B apart, so position p sits
+// at p*16 bytes), and every tap's A operand is the same buffer with the
+// descriptor start moved by shift*16 bytes.  Loader work per channel block
+// drops from hf*wf*128 positions to ~128 + (hf-1)*Wp, and the MMA issuer
+// runs all taps of a block back to back.  Positions that fall on padding
+// columns/rows or between images produce junk outputs that are not stored.
+template <int PASSES, int MH>
+__global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_constant__ TcParams p) {
+  constexpr int LOADERS = THREADS - 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = p.stages;                            // filter-tile ring depth
+
+  const int TP = TILE_P * MH;                        // output positions per tile
+  const uint32_t a_plane = (uint32_t)p.halo * 16u;   // bytes of one 4-channel K-core plane
+  const uint32_t a_bytes = a_plane * 4u;             // one A plane (hi or lo): 16 channels
+  const uint32_t a_buf = a_bytes * (PASSES == 3 ? 2u : 1u);
+  const uint32_t b_plane = (uint32_t)p.NF * BC * 4;  // one filter plane (hi or lo)
+  const uint32_t b_stage = b_plane * (PASSES == 3 ? 2u : 1u);
+  uint8_t *bring = smem + 2 * a_buf;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(bring + (size_t)S * b_stage);
+  // bars: [0,S) b_full (hi landed), [S,2S) b_ready (lo split), [2S,3S) b_empty,
+  //       3S+{0,1} a_full, 3S+{2,3} a_empty, 3S+4 accum
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 5);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int mt = blockIdx.x % p.mtiles;
+  const long long pt = blockIdx.x / p.mtiles;
+  const int m0 = mt * p.NF;
+  const long long q0 = pt * TP;
+  const int cb_per_split = p.kb_per_split / p.taps;
+  const int cb_base = blockIdx.y * cb_per_split;
+  const int NCB = min(p.cblocks - cb_base, cb_per_split);
+  const int KB = NCB * p.taps;
+  const uint32_t smem_base = smem_u32(smem);
+  const uint32_t bring_base = smem_u32(bring);
+  const uint32_t bar_base = smem_u32(bars);
+  auto b_full = [&](int s) { return bar_base + 8u * s; };
+  auto b_ready = [&](int s) { return bar_base + 8u * (S + s); };
+  auto b_empty = [&](int s) { return bar_base + 8u * (2 * S + s); };
+  auto a_full = [&](int b) { return bar_base + 8u * (3 * S + b); };
+  auto a_empty = [&](int b) { return bar_base + 8u * (3 * S + 2 + b); };
+  const uint32_t accum_bar = bar_base + 8u * (3 * S + 4);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; s++) {
+      mbar_init(b_full(s), 1);
+      mbar_init(b_ready(s), LOADERS / 32);
+      mbar_init(b_empty(s), 1);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(a_full(b), LOADERS / 32);
+      mbar_init(a_empty(b), 1);
+    }
+    mbar_init(accum_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_d = *tmem_slot;
+  if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 64) p.dbg[11] = (unsigned)clock64();
+  // TMEM columns: main accumulator of half h at h*NF, 3xTF32 correction at (MH+h)*NF
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == 0) {
+    const bool leader = elect_one();
+    {
+      // ------------------------------------------- filter-tile (hi plane) bulk copies
+      const bool prof = p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && leader;
+      unsigned long long qt_wait = 0;
+      const unsigned long long qt_start = prof ? clock64() : 0;
+      for (int kb = 0; kb < KB; kb++) {
+        const int s = kb % S;
+        const unsigned long long c0 = prof ? clock64() : 0;
+        if (kb >= S) mbar_wait(b_empty(s), ((kb / S) - 1) & 1, p.spin_limit, p.dbg, 0x110000u | kb);
+        if (prof) qt_wait += clock64() - c0;
+        const uint32_t bytes = (PASSES == 3 && !p.bsplit) ? b_stage : b_plane;
+        const float *src = p.wt + ((long long)(cb_base * p.taps + kb) * p.mtiles + mt) * (bytes / 4);
+        if (leader) {
+          if (p.mode & 8) {
+            mbar_arrive(b_full(s));
+          } else {
+            mbar_expect_tx(b_full(s), bytes);
+            bulk_load(bring_base + (uint32_t)s * b_stage, src, bytes, b_full(s));
+          }
+        }
+        __syncwarp();
+      }
+      if (prof) { p.dbg[5] = (unsigned)qt_wait; p.dbg[6] = (unsigned)(clock64() - qt_start); }
+    }
+  } else if (warp == 1) {
+    const bool leader = elect_one();
+    {
+      // ------------------------------------------------------------ MMA issuer
+      // Descriptors are built once per buffer / stage and advanced by adding
+      // the 16-byte-unit offset to their start-address field (all operand
+      // addresses stay below 256 KB, so the 14-bit field never carries).
+      const bool prof = p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && leader;
+      unsigned long long mt_wait = 0, mt_wait_a = 0;
+      const unsigned long long mt_start = prof ? clock64() : 0;
+      const uint64_t a_desc0 = umma_desc(smem_base, a_plane, 128, LAYOUT_NONE);
+      const uint64_t b_desc0 = umma_desc(bring_base, 128, 512, LAYOUT_NONE);
+      const uint32_t idesc = p.idesc;
+      const uint32_t nf = (uint32_t)p.NF;
+      const int taps = p.taps, wf = p.WF, wp = p.Wp;
+      for (int i = 0; i < NCB; i++) {
+        const int buf = i & 1;
+        unsigned long long c0 = prof ? clock64() : 0;
+        mbar_wait(a_full(buf), (i >> 1) & 1, p.spin_limit, p.dbg, 0x210000u | i);
+        if (prof) mt_wait_a += clock64() - c0;
+        tc_fence_after();
+        const uint64_t a_buf_desc = a_desc0 + ((buf * a_buf) >> 4);
+        int ky = 0, kx = 0;
+        for (int t = 0; t < taps; t++) {
+          const int kb = i * taps + t;
+          const int s = kb % S;
+          c0 = prof ? clock64() : 0;
+          mbar_wait((PASSES == 3 && p.bsplit) ? b_ready(s) : b_full(s), (kb / S) & 1, p.spin_limit, p.dbg,
+                    0x220000u | kb);
+          if (prof) mt_wait += clock64() - c0;
+          tc_fence_after();
+          const uint64_t a0 = a_buf_desc + (uint64_t)((ky * wp + kx) & 0xFFFF);  // tap shift: 16 B per position
+          const uint64_t b0 = b_desc0 + (uint64_t)((s * b_stage) >> 4);
+          if (leader) {
+#pragma unroll
+            for (int k = 0; k < BC / 8; k++) {
+              const uint64_t bh = b0 + k * 16;                       // +256 B per UMMA K-step
+              const uint64_t bl = bh + (b_plane >> 4);
+              const uint64_t ak = a0 + k * (2 * a_plane >> 4);       // +2 K-core planes
+              const uint32_t acc = (kb | k) != 0;
+              // consecutive MMAs target different accumulators (main of every
+              // half, then the correction terms) so their latencies overlap
+#pragma unroll
+              for (int h = 0; h < MH; h++)
+                if (!(p.mode & 2)) umma_tf32(tmem_d + h * nf, ak + h * (TILE_P * 16 >> 4), bh, idesc, acc);
+              if (PASSES == 3) {
+#pragma unroll
+                for (int h = 0; h < MH; h++)
+                  if (!(p.mode & 2)) umma_tf32(tmem_d + (MH + h) * nf, ak + h * (TILE_P * 16 >> 4), bl, idesc, acc);
+#pragma unroll
+                for (int h = 0; h < MH; h++)
+                  if (!(p.mode & 2))
+                    umma_tf32(tmem_d + (MH + h) * nf, ak + h * (TILE_P * 16 >> 4) + (a_bytes >> 4), bh, idesc, 1);
+              }
+            }
+            umma_commit(b_empty(s));
+          }
+          __syncwarp();
+          if (++kx == wf) {
+            kx = 0;
+            ++ky;
+          }
+        }
+        if (leader) umma_commit(a_empty(buf));  // the halo buffer is free once this block's MMAs have read it
+        __syncwarp();
+      }
+      if (leader) umma_commit(accum_bar);
+      if (prof) { p.dbg[3] = (unsigned)mt_wait; p.dbg[4] = (unsigned)mt_wait_a; p.dbg[2] = (unsigned)(clock64() - mt_start); }
+    }
+  } else {
+    // --------------------------------------- halo loaders (+ filter lo planes)
+    // halo item = (position, 4-channel group): 4 strided loads, one 16-byte
+    // store (+ the lo twin).  Consecutive lanes take consecutive positions
+    // (coalesced rows of the input).
+    const int lt = threadIdx.x - 64;
+    const int items = p.halo * 4;
+    const float *xg = p.x;
+    const bool prof = p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lt == 0;
+    unsigned long long lt_wait = 0, lt_fill = 0;
+    const unsigned long long lt_start = prof ? clock64() : 0;
+    for (int i = 0; i < NCB; i++) {
+      const int buf = i & 1;
+      unsigned long long c0 = prof ? clock64() : 0;
+      if (i >= 2) {
+        if (lane == 0) mbar_wait(a_empty(buf), ((i >> 1) - 1) & 1, p.spin_limit, p.dbg, 0x310000u | i);
+        __syncwarp();
+      }
+      if (prof) { const unsigned long long c = clock64(); lt_wait += c - c0; c0 = c; }
+      const int cbase = (cb_base + i) * BC;
+      const uint32_t sa = smem_base + buf * a_buf;
+      for (int it = lt; it < items; it += LOADERS) {
+        const int j = it / p.halo;          // 4-channel group
+        const int pos = it - j * p.halo;    // halo position
+        const long long pp = q0 + pos;      // flattened padded-stack index
+        const long long r = pp / p.Wp;
+        const int xx = (int)(pp - r * p.Wp) - p.PW;
+        const int n = (int)(r / p.Hp);
+        const int yy = (int)(r - (long long)n * p.Hp) - p.PH;
+        const int c0 = cbase + j * 4;
+        float v[4];
+        const bool ok = n < p.N && yy >= 0 && yy < p.H && xx >= 0 && xx < p.W && !(p.mode & 1);
+        const float *src = xg + ((long long)n * p.C + c0) * p.HW + (long long)yy * p.W + xx;
+        const int nc = ok ? min(4, p.C - c0) : 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) v[e] = e < nc ? __ldg(src + (long long)e * p.HW) : 0.0f;
+        const uint32_t dst = sa + (uint32_t)j * a_plane + (uint32_t)pos * 16u;
+        sts128(dst, make_float4(v[0], v[1], v[2], v[3]));
+        if (PASSES == 3)
+          sts128(dst + a_bytes, make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3])));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full(buf));
+      if (prof) lt_fill += clock64() - c0;
+      if (PASSES == 3 && p.bsplit) {
+        // lo planes of this block's filter tiles, as they land
+        for (int t = 0; t < p.taps; t++) {
+          const int kb = i * p.taps + t;
+          const int s = kb % S;
+          if (lane == 0) mbar_wait(b_full(s), (kb / S) & 1, p.spin_limit, p.dbg, 0x320000u | kb);
+          __syncwarp();
+          const uint32_t sb = bring_base + (uint32_t)s * b_stage;
+          for (uint32_t o = lt * 16u; o < b_plane; o += LOADERS * 16u) {
+            const float4 a = lds128(sb + o);
+            sts128(sb + b_plane + o, make_float4(tf32_lo(a.x), tf32_lo(a.y), tf32_lo(a.z), tf32_lo(a.w)));
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(b_ready(s));
+        }
+      }
+    }
+    if (prof) { p.dbg[7] = (unsigned)lt_wait; p.dbg[8] = (unsigned)lt_fill; p.dbg[13] = (unsigned)(clock64() - lt_start); }
+    // ------------------------------------------------------------------ epilogue
+    const unsigned long long e0 = prof ? clock64() : 0;
+    if (lane == 0) mbar_wait(accum_bar, 0, p.spin_limit, p.dbg, 0x410000u);
+    __syncwarp();
+    tc_fence_after();
+    if (prof) p.dbg[9] = (unsigned)(clock64() - e0);
+    const int q = warp & 3;
+    const int colgrp = (warp - 2) >> 2;
+    constexpr int COLGRPS = LOADERS / 128;
+    const int mlim = min(p.NF, p.M - m0);
+    float *dst = p.splits > 1 ? p.partials + (long long)blockIdx.y * p.part_stride : p.y;
+    for (int h = 0; h < MH; h++) {
+      const int row = q * 32 + lane;
+      const long long qq = q0 + h * TILE_P + row;
+      const long long r = qq / p.Wp;
+      const int x = (int)(qq - r * p.Wp);
+      const int n = (int)(r / p.Hp);
+      const int y = (int)(r - (long long)n * p.Hp);
+      const bool valid = n < p.N && y < p.Ho && x < p.Wo;
+      const long long obase = ((long long)n * p.M + m0) * p.HoWo + (long long)y * p.Wo + x;
+      for (int j0 = colgrp * 32; j0 < p.NF; j0 += 32 * COLGRPS) {
+        uint32_t rr[32];
+        tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + h * p.NF + j0, rr);
+        if (PASSES == 3) {
+          uint32_t c[32];
+          tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + (MH + h) * p.NF + j0, c);
+#pragma unroll
+          for (int j = 0; j < 32; j++) rr[j] = __float_as_uint(__uint_as_float(rr[j]) + __uint_as_float(c[j]));
+        }
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < 32; j++)
+            if (j0 + j < mlim) dst[obase + (long long)(j0 + j) * p.HoWo] = __uint_as_float(rr[j]);
+        }
+      }
+    }
+  }
+  if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 64) p.dbg[10] = (unsigned)clock64();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

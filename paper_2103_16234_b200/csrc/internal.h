@@ -29,7 +29,10 @@ struct TileChoice {
 
 // Tensor-core implicit-GEMM plan (conv_tc.cu / conv_tc.cuh).
 struct TcPlan {
-  int xb = 0;        // chunk width XW in output columns (32, 16 or 8; chunk = 32/XW rows)
+  int xb = 0;        // gather mode: chunk width XW in output columns (32, 16 or 8; chunk = 32/XW rows)
+  int halo = 0;      // halo mode (stride 1): staged positions per tile (0 = gather mode)
+  int mh = 1;        // halo mode: 128-position M halves per tile
+  int wplanes = 1;   // pre-tiled filter planes streamed from HBM/L2 (gather 3xTF32: hi + lo)
   int nf = 0;        // output channels per tile (UMMA N)
   int mtiles = 0;
   int stages = 0, stage_bytes = 0, smem_bytes = 0, tmem_cols = 0;
@@ -43,7 +46,8 @@ struct TcPlan {
 bool tc_supported(const Geom &g);
 bool tc_flat(const Geom &g);
 long long tc_workspace_bytes(const Geom &g, const TcPlan &pl);
-bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced_splits, TcPlan *out);
+bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced_splits, TcPlan *out,
+             int forced_mode = 0);
 long long tc_filter_bytes(const Geom &g, const TcPlan &pl);
 cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const float *w, float *y, void *workspace,
                       long long ws_bytes, cudaStream_t stream);

@@ -57,7 +57,7 @@ class ConvLayer:
     """A resolved forward convolution for one configuration."""
 
     def __init__(self, cfg: ConvConfig, engine: str = "fused", family: int = -1, splits: int = 0,
-                 filters_per_tile: int = 0):
+                 filters_per_tile: int = 0, tc_mode: int = 0):
         if engine not in nat.ENGINES:
             raise ValueError(f"unknown engine {engine!r}")
         if engine == "twostage" and cfg.stride != 1:
@@ -75,6 +75,7 @@ class ConvLayer:
             self._tc = nat.TcPlanC()
             self._tc.filters_per_tile = int(filters_per_tile)
             self._tc.splits = int(splits)
+            self._tc.mode = int(tc_mode)
             nat.check(self._lib.b2c_tc_select_tiles(ctypes.byref(self._desc), self._engine_id, ctypes.byref(self._tc)))
         else:
             e = nat.ENGINE_TWOSTAGE if engine == "twostage" else nat.ENGINE_FUSED
@@ -93,7 +94,8 @@ class ConvLayer:
     def family(self) -> str:
         if self.tensor_core:
             t = self._tc
-            return (f"{self.engine}_x{t.pixels_per_chunk}_n{t.filters_per_tile}_s{t.stages}_k{t.splits}"
+            shape = f"h{t.halo_positions}" if t.mode == 2 else f"x{t.pixels_per_chunk}"
+            return (f"{self.engine}_{shape}_n{t.filters_per_tile}_s{t.stages}_k{t.splits}"
                     + ("_flat" if t.flattened else ""))
         return self._lib.b2c_family_name(self._tiles.family).decode()
 

@@ -296,24 +296,39 @@ def test_tensor_core_planner_covers_every_baseline_layer(native):
                 for engine in ("tf32x3", "tf32"):
                     p = _tc_plan(native, cfg, engine)
                     assert p.passes == (3 if engine == "tf32x3" else 1)
-                    assert p.pixels_per_chunk in (8, 16, 32) and p.filters_per_tile % 16 == 0
+                    assert p.pixels_per_chunk in ((8, 16, 32) if p.mode == 1 else (0,)) and p.filters_per_tile % 16 == 0
                     assert 16 <= p.filters_per_tile <= 256 and p.filter_tiles * p.filters_per_tile >= cfg.m
                     assert p.stages >= 2 and p.smem_bytes <= 227 * 1024
-                    cols = p.filters_per_tile * (2 if engine == "tf32x3" else 1)
+                    cols = p.filters_per_tile * (2 if engine == "tf32x3" else 1) * (p.m_halves if p.mode == 2 else 1)
                     assert cols <= p.tmem_columns <= 512 and p.tmem_columns & (p.tmem_columns - 1) == 0
                     flat = cfg.hf == cfg.wf == 1 and cfg.stride == 1 and cfg.pad_h == cfg.pad_w == 0
                     assert bool(p.flattened) == flat
-                    width = ho * wo if flat else wo
-                    rows = 1 if flat else ho
-                    xw = p.pixels_per_chunk
-                    chunks = cfg.n * -(-rows // (32 // xw)) * -(-width // xw)
-                    assert p.grid == -(-chunks // 4) * p.filter_tiles * p.splits, (wl, cfg.name)
-                    planes = 2 if engine == "tf32x3" else 1
                     kb = -(-cfg.c // 16) * cfg.hf * cfg.wf
-                    assert 1 <= p.splits <= kb
+                    assert p.mode in (1, 2)
+                    if p.mode == 1:  # gather: 128-pixel tiles of 32-pixel chunks
+                        width = ho * wo if flat else wo
+                        rows = 1 if flat else ho
+                        xw = p.pixels_per_chunk
+                        chunks = cfg.n * -(-rows // (32 // xw)) * -(-width // xw)
+                        tiles = -(-chunks // 4)
+                        assert 1 <= p.splits <= kb
+                        kbps = -(-kb // p.splits)
+                    else:  # halo: 128 positions of the flattened padded stack
+                        assert cfg.stride == 1
+                        hp, wp = cfg.h + 2 * cfg.pad_h, cfg.w + 2 * cfg.pad_w
+                        mh = p.m_halves
+                        assert mh in (1, 2)
+                        assert p.halo_positions == -(-(128 * mh + (cfg.hf - 1) * wp + cfg.wf - 1) // 8) * 8
+                        tiles = -(-(cfg.n * hp * wp) // (128 * mh))
+                        cbl = -(-cfg.c // 16)
+                        assert 1 <= p.splits <= cbl
+                        kbps = -(-cbl // p.splits) * cfg.hf * cfg.wf
+                    assert p.grid == tiles * p.filter_tiles * p.splits, (wl, cfg.name)
+                    planes = 2 if engine == "tf32x3" else 1
                     if engine == "tf32x3":
-                        assert -(-kb // p.splits) <= 72  # <= 1152 products per split (accuracy rule)
-                    filt = 4 * kb * 16 * p.filter_tiles * p.filters_per_tile * planes
+                        assert kbps <= max(72, cfg.hf * cfg.wf)  # <= 1152 products per split (accuracy rule)
+                    wpl = planes
+                    filt = 4 * kb * 16 * p.filter_tiles * p.filters_per_tile * wpl
                     part = 4 * p.splits * cfg.n * cfg.m * ho * wo if p.splits > 1 else 0
                     assert p.workspace_bytes == -(-filt // 256) * 256 + part
 
