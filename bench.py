@@ -316,28 +316,33 @@ def time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank):
 
 
 def e2e_run(lib, nat, cfgs, xs, ws, ys, engine_id, steps, world, device, local_rank):
-    """Same metric through the host-buffer C-ABI drop-in: every step copies each
+    """Same metric through the host-buffer C-ABI: every step copies each
     layer's input and filters from pinned host memory, convolves, and copies
-    the output back (synchronous per layer).  Wall time, max over ranks."""
+    the output back, all layers of the step in one b2c_conv_host_layers call
+    (copies and compute of consecutive layers overlap on three streams).
+    Wall time, max over ranks."""
     import ctypes
 
     import torch
     import torch.distributed as dist
 
-    pinned = []
+    n = len(cfgs)
+    descs = (nat.ConvDesc * n)()
+    xp, wp, yp = ((ctypes.c_void_p * n)() for _ in range(3))
+    keep = []
     h2d = d2h = 0
-    for c, x, w, y in zip(cfgs, xs, ws, ys):
+    for i, (c, x, w, y) in enumerate(zip(cfgs, xs, ws, ys)):
         hx = torch.empty(x.shape, dtype=torch.float32, pin_memory=True).copy_(x)
         hw = torch.empty(w.shape, dtype=torch.float32, pin_memory=True).copy_(w)
         hy = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
-        pinned.append((nat.desc(c), hx, hw, hy))
+        keep += [hx, hw, hy]
+        descs[i] = nat.desc(c)
+        xp[i], wp[i], yp[i] = hx.data_ptr(), hw.data_ptr(), hy.data_ptr()
         h2d += hx.numel() * 4 + hw.numel() * 4
         d2h += hy.numel() * 4
 
     def e2e_step():
-        for d, hx, hw, hy in pinned:
-            nat.check(lib.b2c_conv_host(ctypes.byref(d), hx.data_ptr(), hw.data_ptr(), hy.data_ptr(), engine_id,
-                                        None, None, 1 << 62, local_rank, None))
+        nat.check(lib.b2c_conv_host_layers(n, descs, xp, wp, yp, engine_id, local_rank))
 
     e2e_step()
     if world > 1:
@@ -354,7 +359,8 @@ def e2e_run(lib, nat, cfgs, xs, ws, ys, engine_id, steps, world, device, local_r
     return {"value": round(flops * world * steps / dt / 1e9, 3), "unit": "GFLOP/s",
             "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
             "ms_per_step": round(1e3 * dt / steps, 3),
-            "path": "b2c_conv_host (C ABI, pinned host buffers, synchronous per layer)"}
+            "path": "b2c_conv_host_layers (C ABI, pinned host buffers; H2D/compute/D2H of consecutive layers "
+                    "overlapped on 3 streams)"}
 
 
 TC_TOLERANCE = {"tf32x3": "relative_error vs conv_naive_f64 <= 1e-5*max(1, K/4096) (the fp32 gate)",
@@ -454,7 +460,8 @@ def main():
     # e2e: host buffers through the C-ABI drop-in (H2D x,w + kernel + D2H y per layer)
     e2e = None
     if args.e2e_steps > 0:
-        e2e = e2e_run(lib, nat, cfgs, xs, ws, ys, nat.ENGINES[args.engine], args.e2e_steps, world, device,
+        e2e_engine = args.engine if args.engine != "twostage" else "fused"
+        e2e = e2e_run(lib, nat, cfgs, xs, ws, ys, nat.ENGINES[e2e_engine], args.e2e_steps, world, device,
                       local_rank)
 
     # the optional tensor-core variant (tcgen05 implicit GEMM), reported separately

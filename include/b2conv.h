@@ -202,6 +202,12 @@ b2c_status b2c_conv2d_forward_tc(const b2c_conv_desc *d, const float *x, const f
  * out->filters_per_tile / out->splits > 0 on entry are forced. */
 b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_plan *out);
 
+/* Register a measured tensor-core plan (tools/autotune.py) for an exact shape:
+ * the planner then uses (mode, filters_per_tile, splits) for it.  The Python
+ * package registers paper_2103_16234_b200/tuned_plans.json at import. */
+b2c_status b2c_register_tuned_tc_plan(const b2c_conv_desc *d, int32_t engine, int32_t mode, int32_t filters_per_tile,
+                                      int32_t splits);
+
 /* twostage.conv_twostage (twostage.py:208-239): preconditions in the
  * reference's order, then stage 1 (+ stage 2 unless 1x1) with the reference's
  * rounding order.  `plan` may be NULL (plan_launch default).  `workspace`
@@ -231,6 +237,16 @@ b2c_status b2c_stage2_sum(const b2c_conv_desc *d, const float *partials, float *
 b2c_status b2c_conv_host(const b2c_conv_desc *d, const float *x_host, const float *w_host, float *y_host,
                          int32_t engine, const b2c_launch_plan *plan, const b2c_device_model *dev,
                          int64_t workspace_limit, int32_t device, b2c_run_stats *stats);
+
+/* A sequence of independent layers (e.g. one inference pass over a network's
+ * convolutions) from host buffers: H2D copies, convolutions and D2H copies of
+ * consecutive layers overlap on three streams (three device slots, event
+ * ordered); synchronous on return.  Pinned host memory gives full PCIe
+ * overlap.  engine: B2C_ENGINE_FUSED, _TF32X3 or _TF32.  The batched form of
+ * b2c_conv_host for harness loops like the reference's run_bench
+ * (bench.py:91-163), which convolves one layer after another. */
+b2c_status b2c_conv_host_layers(int32_t count, const b2c_conv_desc *descs, const float *const *x_host,
+                                const float *const *w_host, float *const *y_host, int32_t engine, int32_t device);
 
 /* Host-buffer stage 1 / stage 2 (used by the drop-in stage1_scalar_prods /
  * stage2_sum). */

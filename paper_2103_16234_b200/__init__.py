@@ -3,7 +3,8 @@ arXiv 2103.16234), a drop-in for convkit's forward-convolution entry point.
 
 Host API (numpy in/out, reference signatures and exceptions):
     conv_twostage, stage1_scalar_prods, stage2_sum, workspace_bytes,
-    conv_forward (any stride), RunStats, PartialSums, DEFAULT_WORKSPACE_LIMIT
+    conv_forward (any stride), conv_forward_layers (pipelined sequence),
+    RunStats, PartialSums, DEFAULT_WORKSPACE_LIMIT
 Device API (torch CUDA tensors, current stream):
     conv2d, ConvLayer
 Shapes, tensors, plans, errors:
@@ -20,8 +21,8 @@ from .errors import (ConvKitError, DeviceError, FormatError, InvalidConfig, Inva
 from .execmodel import (DeviceModel, LaunchPlan, TilePlan, block_position_ranges, family_names,
                         matching_families, plan_launch, select_tiles, theoretical_reuse, validate_plan)
 from .tensor import Tensor4, load_tensor, make_tensor, read_padded, save_tensor
-from .twostage import (DEFAULT_WORKSPACE_LIMIT, PartialSums, RunStats, conv_forward, conv_twostage,
-                       stage1_scalar_prods, stage2_sum, workspace_bytes)
+from .twostage import (DEFAULT_WORKSPACE_LIMIT, PartialSums, RunStats, conv_forward, conv_forward_layers,
+                       conv_twostage, stage1_scalar_prods, stage2_sum, workspace_bytes)
 from .engine import ConvLayer, conv2d
 
 __version__ = "0.1.0"

@@ -83,6 +83,8 @@ SIGNATURES = {
     "b2c_conv2d_forward_tc": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, ctypes.c_void_p, ctypes.c_int64,
                                              ctypes.c_int32, _P(TcPlanC), ctypes.c_void_p]),
     "b2c_tc_select_tiles": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, _P(TcPlanC)]),
+    "b2c_register_tuned_tc_plan": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                  ctypes.c_int32]),
     "b2c_conv_twostage": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _fp, ctypes.c_int64, _P(LaunchPlanC),
                                          _P(DeviceModelC), ctypes.c_int64, ctypes.c_void_p, _P(RunStatsC)]),
     "b2c_stage1_scalar_prods": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _P(LaunchPlanC), _P(DeviceModelC),
@@ -90,6 +92,8 @@ SIGNATURES = {
     "b2c_stage2_sum": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, ctypes.c_void_p, _P(RunStatsC)]),
     "b2c_conv_host": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, ctypes.c_int32, _P(LaunchPlanC),
                                      _P(DeviceModelC), ctypes.c_int64, ctypes.c_int32, _P(RunStatsC)]),
+    "b2c_conv_host_layers": (ctypes.c_int, [ctypes.c_int32, _P(ConvDesc), _P(ctypes.c_void_p), _P(ctypes.c_void_p),
+                                            _P(ctypes.c_void_p), ctypes.c_int32, ctypes.c_int32]),
     "b2c_stage1_host": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _P(LaunchPlanC), _P(DeviceModelC),
                                        ctypes.c_int64, ctypes.c_int32, _P(RunStatsC)]),
     "b2c_stage2_host": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, ctypes.c_int32, _P(RunStatsC)]),
@@ -141,6 +145,11 @@ def _register_tuned(l) -> None:
         return
     names = [l.b2c_family_name(i).decode() for i in range(l.b2c_num_families())]
     for e in entries:
+        if e.get("engine") in ("tf32x3", "tf32"):
+            d = ConvDesc(*[int(v) for v in e["desc"]])
+            l.b2c_register_tuned_tc_plan(ctypes.byref(d), ENGINES[e["engine"]], int(e["mode"]), int(e["nf"]),
+                                         int(e["splits"]))
+            continue
         if e.get("family") not in names:
             continue
         d = ConvDesc(*[int(v) for v in e["desc"]])

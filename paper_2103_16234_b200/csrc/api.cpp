@@ -472,6 +472,17 @@ b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_pl
   return B2C_OK;
 }
 
+b2c_status b2c_register_tuned_tc_plan(const b2c_conv_desc *d, int32_t engine, int32_t mode, int32_t filters_per_tile,
+                                      int32_t splits) {
+  b2c_status st = check_config(d, nullptr);
+  if (st != B2C_OK) return st;
+  b2c::Geom g = geom_of(d);
+  b2c::TcPlan pl;
+  if ((st = tc_plan_of(d, g, engine, filters_per_tile, splits, &pl, mode)) != B2C_OK) return st;  // must be runnable
+  b2c::register_tuned_tc(g, engine == B2C_ENGINE_TF32X3 ? 3 : 1, mode, filters_per_tile, splits);
+  return B2C_OK;
+}
+
 b2c_status b2c_conv2d_forward_tc(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
                                  int64_t workspace_size, int32_t engine, const b2c_tc_plan *tiles, void *stream) {
   b2c_status st = check_config(d, nullptr);
@@ -613,6 +624,107 @@ b2c_status b2c_conv_host(const b2c_conv_desc *d, const float *x_host, const floa
   e = cudaMemcpyAsync(y_host, dy, yb, cudaMemcpyDeviceToHost, b->stream);
   if (e != cudaSuccess) return cuda_fail(e, "device-to-host copy");
   return sync_and_check(b->stream, "convolution");
+}
+
+// Pipelined host-buffer path over a sequence of layers: slot i%3 holds layer
+// i's device buffers; H2D copies (own stream), convolutions (own stream) and
+// D2H copies (own stream) of consecutive layers overlap, ordered by events.
+namespace {
+struct Pipeline {
+  static constexpr int kSlots = 3;
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  cudaEvent_t loaded[kSlots] = {}, computed[kSlots] = {}, drained[kSlots] = {};
+  DeviceBuffers slot[kSlots];
+  bool used[kSlots] = {};
+};
+thread_local std::unordered_map<int, Pipeline> t_pipes;
+
+b2c_status pipeline_of(int32_t device, Pipeline **out) {
+  if (device >= 0) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  Pipeline &pl = t_pipes[cur];
+  if (!pl.h2d) {
+    cudaError_t e = cudaSuccess;
+    for (cudaStream_t *st : {&pl.h2d, &pl.comp, &pl.d2h})
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(st, cudaStreamNonBlocking);
+    for (int i = 0; i < Pipeline::kSlots && e == cudaSuccess; i++) {
+      for (cudaEvent_t *ev : {&pl.loaded[i], &pl.computed[i], &pl.drained[i]})
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "pipeline setup");
+  }
+  *out = &pl;
+  return B2C_OK;
+}
+}  // namespace
+
+b2c_status b2c_conv_host_layers(int32_t count, const b2c_conv_desc *descs, const float *const *x_host,
+                                const float *const *w_host, float *const *y_host, int32_t engine, int32_t device) {
+  if (count < 0 || (count > 0 && (!descs || !x_host || !w_host || !y_host)))
+    return fail(B2C_INVALID_ARGUMENT, "null layer arrays");
+  if (engine != B2C_ENGINE_FUSED && engine != B2C_ENGINE_TF32X3 && engine != B2C_ENGINE_TF32)
+    return fail(B2C_INVALID_ARGUMENT, "b2c_conv_host_layers runs the fused or tensor-core engines, got %d", engine);
+  b2c_status st;
+  for (int i = 0; i < count; i++) {
+    if ((st = check_config(&descs[i], nullptr)) != B2C_OK) return st;
+    if ((st = check_sizes(geom_of(&descs[i]))) != B2C_OK) return st;
+    if (!x_host[i] || !w_host[i] || !y_host[i]) return fail(B2C_INVALID_ARGUMENT, "null tensor pointer (layer %d)", i);
+  }
+  Pipeline *pl = nullptr;
+  if ((st = pipeline_of(device, &pl)) != B2C_OK) return st;
+  for (int i = 0; i < count; i++) {
+    const b2c_conv_desc *d = &descs[i];
+    const b2c::Geom g = geom_of(d);
+    const int k = i % Pipeline::kSlots;
+    DeviceBuffers &b = pl->slot[k];
+    // the slot's previous layer must have drained before its buffers are reused
+    if (pl->used[k]) {
+      cudaError_t e = cudaEventSynchronize(pl->drained[k]);
+      if (e != cudaSuccess) return cuda_fail(e, "pipeline drain");
+    }
+    const size_t xb = sizeof(float) * (size_t)g.N * g.C * g.H * g.W;
+    const size_t wb = sizeof(float) * (size_t)g.M * g.C * g.HF * g.WF;
+    const size_t yb = sizeof(float) * (size_t)g.N * g.M * g.HoWo;
+    size_t wsb = 0;
+    b2c::TileChoice tc;
+    b2c::TcPlan tp;
+    if (engine == B2C_ENGINE_FUSED) {
+      if ((st = get_tiles(d, g, false, -1, 0, true, &tc)) != B2C_OK) return st;
+      wsb = (size_t)tc.ws_bytes;
+    } else {
+      if ((st = tc_plan_of(d, g, engine, 0, 0, &tp)) != B2C_OK) return st;
+      wsb = (size_t)b2c::tc_workspace_bytes(g, tp);
+    }
+    if ((st = ensure(b, 0, xb)) || (st = ensure(b, 1, wb)) || (st = ensure(b, 2, yb)) ||
+        (wsb && (st = ensure(b, 4, wsb))))
+      return st;
+    cudaError_t e = cudaMemcpyAsync(b.ptr[0], x_host[i], xb, cudaMemcpyHostToDevice, pl->h2d);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(b.ptr[1], w_host[i], wb, cudaMemcpyHostToDevice, pl->h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(pl->loaded[k], pl->h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(pl->comp, pl->loaded[k], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "host-to-device copy");
+    const float *dx = static_cast<const float *>(b.ptr[0]);
+    const float *dw = static_cast<const float *>(b.ptr[1]);
+    float *dy = static_cast<float *>(b.ptr[2]);
+    if (engine == B2C_ENGINE_FUSED)
+      st = b2c_conv2d_forward(d, dx, dw, dy, wsb ? b.ptr[4] : nullptr, (int64_t)wsb, nullptr, pl->comp);
+    else
+      st = b2c_conv2d_forward_tc(d, dx, dw, dy, b.ptr[4], (int64_t)wsb, engine, nullptr, pl->comp);
+    if (st != B2C_OK) return st;
+    e = cudaEventRecord(pl->computed[k], pl->comp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(pl->d2h, pl->computed[k], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(y_host[i], dy, yb, cudaMemcpyDeviceToHost, pl->d2h);
+    if (e == cudaSuccess) e = cudaEventRecord(pl->drained[k], pl->d2h);
+    if (e != cudaSuccess) return cuda_fail(e, "device-to-host copy");
+    pl->used[k] = true;
+  }
+  for (cudaStream_t sv : {pl->h2d, pl->comp, pl->d2h})
+    if ((st = sync_and_check(sv, "pipelined convolution")) != B2C_OK) return st;
+  return B2C_OK;
 }
 
 b2c_status b2c_stage1_host(const b2c_conv_desc *d, const float *x_host, const float *w_host, float *partials_host,

@@ -7,7 +7,9 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <mutex>
+#include <unordered_map>
 #include <cstdio>
 
 #include "conv_tc.cuh"
@@ -53,9 +55,48 @@ long long tc_workspace_bytes(const Geom &g, const TcPlan &pl) {
   return tc_filter_bytes(g, pl) + partials;
 }
 
+// Measured plans (tools/autotune.py --engines tf32x3,tf32), registered at
+// import by the Python package: exact (shape, passes) -> (mode, nf, splits).
+namespace {
+struct TcKey {
+  int v[11];
+  bool operator==(const TcKey &o) const { return std::memcmp(v, o.v, sizeof(v)) == 0; }
+};
+struct TcKeyHash {
+  size_t operator()(const TcKey &k) const {
+    size_t h = 1469598103934665603ULL;
+    for (int x : k.v) h = (h ^ (size_t)(unsigned)x) * 1099511628211ULL;
+    return h;
+  }
+};
+std::unordered_map<TcKey, std::array<int, 3>, TcKeyHash> g_tc_tuned;
+std::mutex g_tc_tuned_mu;
+TcKey tc_key(const Geom &g, int passes) {
+  return TcKey{{g.N, g.C, g.H, g.W, g.M, g.HF, g.WF, g.S, g.PH, g.PW, passes}};
+}
+}  // namespace
+
+void register_tuned_tc(const Geom &g, int passes, int mode, int nf, int splits) {
+  std::lock_guard<std::mutex> lk(g_tc_tuned_mu);
+  g_tc_tuned[tc_key(g, passes)] = {mode, nf, splits};
+}
+
 bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced_splits, TcPlan *out,
              int forced_mode) {
   if (!tc_supported(g)) return false;
+  if (forced_nf <= 0 && forced_splits <= 0 && forced_mode <= 0 && forced_xb <= 0) {
+    std::array<int, 3> t{0, 0, 0};
+    bool hit = false;
+    {
+      std::lock_guard<std::mutex> lk(g_tc_tuned_mu);
+      auto it = g_tc_tuned.find(tc_key(g, passes));
+      if (it != g_tc_tuned.end()) {
+        t = it->second;
+        hit = true;
+      }
+    }
+    if (hit && plan_tc(g, passes, t[1], 0, t[2], out, t[0])) return true;
+  }
   const bool flat = tc_flat(g);
   const int wo = flat ? g.HoWo : g.Wo;
   const int ho = flat ? 1 : g.Ho;

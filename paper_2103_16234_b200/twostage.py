@@ -183,3 +183,31 @@ def conv_forward(inp: Tensor4, filters: Tensor4, cfg: ConvConfig, *, gpu: int = 
                                  out.ctypes.data, nat.ENGINES[engine], None, None, 0, int(gpu), None)
     nat.check(st)
     return Tensor4(out)
+
+
+def conv_forward_layers(layers, *, engine: str = "fused", gpu: int = -1) -> list[Tensor4]:
+    """A sequence of independent convolutions ``[(inp, filters, cfg), ...]``
+    (e.g. every layer of a network for one batch) from host buffers: the
+    host-to-device copies, the convolutions and the device-to-host copies of
+    consecutive layers overlap (b2c_conv_host_layers).  The batched form of
+    calling ``conv_forward`` in a loop, as the reference harness does
+    (bench.py:91-163)."""
+    if engine not in ("fused", "tf32x3", "tf32"):
+        raise ValueError(f"conv_forward_layers runs the fused or tensor-core engines, got {engine!r}")
+    n = len(layers)
+    descs = (nat.ConvDesc * max(n, 1))()
+    outs, keep = [], []
+    xp = (ctypes.c_void_p * max(n, 1))()
+    wp = (ctypes.c_void_p * max(n, 1))()
+    yp = (ctypes.c_void_p * max(n, 1))()
+    for i, (inp, filters, cfg) in enumerate(layers):
+        _check_operands(inp, filters, cfg, stride1=False)
+        descs[i] = nat.desc(cfg)
+        ho, wo = output_dims(cfg)
+        out = np.empty((cfg.n, cfg.m, ho, wo), dtype=np.float32)
+        outs.append(Tensor4(out))
+        keep += [inp.data, filters.data, out]
+        xp[i], wp[i], yp[i] = inp.data.ctypes.data, filters.data.ctypes.data, out.ctypes.data
+    st = nat.lib().b2c_conv_host_layers(n, descs, xp, wp, yp, nat.ENGINES[engine], int(gpu))
+    nat.check(st)
+    return outs

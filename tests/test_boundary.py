@@ -355,3 +355,26 @@ def test_tensor_core_planner_forced_tiles_and_errors(native):
     p.splits = 3
     assert native.b2c_tc_select_tiles(ctypes.byref(nat.desc(cfg)), nat.ENGINE_TF32, ctypes.byref(p)) == nat.OK
     assert p.splits == 3
+
+
+# --- harness I/O compatibility ------------------------------
+
+def test_harness_csv_header_is_reference_prefix_and_skips(tmp_path):
+    from paper_2103_16234_b200 import harness as H
+
+    assert H.CSV_HEADER == ("config,algorithm,batch,repeats,mean_us,min_us,stddev_us,speedup,validated,"
+                            "workspace_bytes,txn_per_warp")  # convkit bench.py:37
+    s2 = pk.ConvConfig("s2", n=1, c=3, h=9, w=9, m=4, hf=3, wf=3, stride=2, pad_h=1, pad_w=1)
+    assert H.skip_reason("twostage", s2) == "Unsupported: stride"
+    big = pk.ConvConfig("big", n=128, c=64, h=224, w=224, m=64, hf=3, wf=3, pad_h=1, pad_w=1)
+    assert H.skip_reason("twostage", big) == "WorkspaceExceeded"
+    assert H.skip_reason("tf32x3", s2) is None and H.skip_reason("fused", big) is None
+    with pytest.raises(pk.ConvKitError):
+        H.skip_reason("winograd", s2)
+    rec = H.BenchRecord(config="s2", algorithm="twostage", batch=1, skipped=True, skip_reason="Unsupported: stride")
+    out = tmp_path / "r.csv"
+    H.emit_report([rec], out)
+    lines = out.read_text().splitlines()
+    assert lines[0].startswith(H.CSV_HEADER + ",") and lines[1].startswith("s2,twostage,1,0,,,,,skipped(Unsupported: stride)")
+    with pytest.raises(pk.ConvKitError):
+        H.emit_report([], out)

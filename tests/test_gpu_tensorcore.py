@@ -202,3 +202,30 @@ def test_tensor_core_graph_capture_and_c_abi_plan():
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(y, want)
+
+
+@pytest.mark.parametrize("engine", ("fused", "tf32x3"))
+def test_pipelined_host_layers_match_single_calls(engine):
+    """b2c_conv_host_layers (H2D / compute / D2H of consecutive layers
+    overlapped) returns exactly what one conv_forward call per layer does."""
+    cfgs = [pk.ConvConfig(f"l{i}", n=2, c=c, h=h, w=h, m=m, hf=f, wf=f, pad_h=f // 2, pad_w=f // 2, stride=s)
+            for i, (c, h, m, f, s) in enumerate([(16, 14, 24, 3, 1), (24, 7, 40, 1, 1), (40, 9, 8, 5, 1),
+                                                 (8, 15, 16, 3, 2), (16, 28, 32, 1, 1)])]
+    layers = [(pk.make_tensor(pk.input_dims(c), "uniform", seed=10 + i),
+               pk.make_tensor(pk.filter_dims(c), "uniform", seed=20 + i), c) for i, c in enumerate(cfgs)]
+    outs = pk.conv_forward_layers(layers, engine=engine)
+    for (x, w, c), o in zip(layers, outs):
+        assert o.data.tobytes() == pk.conv_forward(x, w, c, engine=engine).data.tobytes(), c.name
+
+
+def test_harness_run_bench_validates_every_engine(tmp_path):
+    from paper_2103_16234_b200 import harness as H
+
+    cfgs = pk.preset_configs()[:3] + pk.preset_configs()[-2:]
+    recs = H.run_bench(cfgs, ("fused", "twostage", "tf32x3", "tf32"), (1, 2), repeats=3)
+    assert len(recs) == len(cfgs) * 2 * 4
+    assert all(r.validated for r in recs if not r.skipped), [(r.config, r.algorithm, r.max_rel_error) for r in recs]
+    assert all(r.max_rel_error == 0.0 for r in recs if r.algorithm == "twostage")  # it is the reference
+    H.emit_report(recs, tmp_path / "r.csv")
+    H.emit_report(recs, tmp_path / "r.md", "md")
+    assert (tmp_path / "r.csv").read_text().count("\n") == len(recs) + 1

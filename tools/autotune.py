@@ -34,18 +34,60 @@ def time_layer(L, x, w, y, reps=20):
     return sorted(ts)[1]
 
 
+def tc_accurate(cfg, L):
+    """3xTF32 accuracy rule: <= 72 k-blocks of 16 channels per
+    TMEM accumulator (halo mode keeps whole channel blocks, so at least one)."""
+    t = L._tc
+    cb = -(-cfg.c // 16)
+    taps = cfg.hf * cfg.wf
+    if t.mode == 2:
+        return -(-cb // t.splits) * taps <= max(72, taps)
+    return -(-(cb * taps) // t.splits) <= 72
+
+
+def tune_tc(cfg, eng, x, w, label, desc):
+    auto = ConvLayer(cfg, eng)
+    y = torch.empty(auto.output_shape(), device="cuda")
+    t_auto = time_layer(auto, x, w, y)
+    best = (t_auto, auto._tc.mode, 0, 0, auto.family)
+    seen = {auto.family}
+    for mode in (1, 2):
+        for nf in (0, 32, 64, 96, 128, 192, 256):
+            for sp in (0, 1, 2, 3, 4, 6, 8, 12):
+                try:
+                    L = ConvLayer(cfg, eng, tc_mode=mode, filters_per_tile=nf, splits=sp)
+                except Exception:  # noqa: BLE001
+                    continue
+                if L.family in seen or (eng == "tf32x3" and not tc_accurate(cfg, L)):
+                    continue
+                seen.add(L.family)
+                t = time_layer(L, x, w, y)
+                if t < best[0]:
+                    best = (t, L._tc.mode, L._tc.filters_per_tile, L._tc.splits, L.family)
+    del y
+    if best[2] == 0:
+        return {"layer": label, "desc": desc, "engine": eng, "mode": best[1], "nf": 0, "splits": 0,
+                "plan": best[4], "us": round(best[0], 2), "model_us": round(t_auto, 2)}
+    return {"layer": label, "desc": desc, "engine": eng, "mode": best[1], "nf": best[2], "splits": best[3],
+            "plan": best[4], "us": round(best[0], 2), "model_us": round(t_auto, 2)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workloads", default="c1,c2,c3,c4,c5")
     ap.add_argument("--out", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                                    "paper_2103_16234_b200", "tuned_plans.json"))
     ap.add_argument("--budget-s", type=float, default=1500)
+    ap.add_argument("--engines", default="fused", help="comma list of fused, tf32x3, tf32")
+    ap.add_argument("--batches", default="", help="override the batch sizes per workload (comma list)")
     args = ap.parse_args()
+    engines = args.engines.split(",")
     names = family_names()
     plans, seen = [], set()
     t_start = time.time()
     for wl in args.workloads.split(","):
-        for n in W.WORKLOADS[wl][1]:
+        batches = [int(b) for b in args.batches.split(",")] if args.batches else W.WORKLOADS[wl][1]
+        for n in batches:
             for cfg in W.layers(wl, n):
                 key = cfg.as_tuple()
                 if key in seen:
@@ -55,6 +97,15 @@ def main():
                     break
                 x = torch.rand((cfg.n, cfg.c, cfg.h, cfg.w), device="cuda")
                 w = torch.rand((cfg.m, cfg.c, cfg.hf, cfg.wf), device="cuda")
+                for eng in engines:
+                    if eng != "fused":
+                        rec = tune_tc(cfg, eng, x, w, f"{wl}/{cfg.name}/N{n}", list(key))
+                        if rec:
+                            print(json.dumps(rec), flush=True)
+                            if rec["us"] < rec["model_us"] * 0.97:
+                                plans.append(rec)
+                if "fused" not in engines:
+                    continue
                 auto = ConvLayer(cfg)
                 y = torch.empty(auto.output_shape(), device="cuda")
                 t_auto = time_layer(auto, x, w, y)
