@@ -20,10 +20,16 @@
 //   epilogue    = STG.128 of 4 consecutive pixels per channel.
 #pragma once
 
+#include <type_traits>
+
 #include "conv_kernel.cuh"
 
 namespace b2c {
 
+// VEC = false: planes with H*W % 4 != 0 (7x7 GoogLeNet 5a/5b, 27x27): the
+// same register/shared mapping, pixels staged by 4-byte cp.async with a
+// per-pixel image offset (a 4-pixel group may straddle two images) and
+// scalar output stores.
 template <int WM, int WP, int BC>
 struct Vec1x1Tile {
   static constexpr int BM = 32 * WM;
@@ -37,7 +43,7 @@ struct Vec1x1Tile {
   static constexpr int MIN_BLOCKS = NT >= 512 ? 1 : 512 / NT;
 };
 
-template <int WM, int WP, int BC>
+template <int WM, int WP, int BC, bool VEC = true>
 __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP, BC>::MIN_BLOCKS)
     conv1x1_vec_kernel(const KParams p) {
   using T = Vec1x1Tile<WM, WP, BC>;
@@ -60,7 +66,9 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP,
 
   // per-thread 16-byte pixel groups of a chunk: global offset relative to the
   // chunk's first channel (or -1 beyond the last pixel)
-  long long xoff[T::XG_PER_THREAD];
+  constexpr int PX = VEC ? 1 : 4;  // offsets per 4-pixel group
+  using Off = typename std::conditional<VEC, long long, int>::type;  // !VEC: the planner guarantees n*c*h*w < 2^31
+  Off xoff[T::XG_PER_THREAD][PX];
   int xdst[T::XG_PER_THREAD];
 #pragma unroll
   for (int k = 0; k < T::XG_PER_THREAD; k++) {
@@ -69,11 +77,15 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP,
     const int pg = gi - c * (BP / 4);
     const int q = q0 + 4 * pg;
     xdst[k] = gi < T::XG ? c * BP + 4 * pg : -1;
-    if (gi < T::XG && q < p.Q) {
-      const int n = q / hw;
-      xoff[k] = (long long)n * chw + (long long)c * hw + (q - n * hw);
-    } else {
-      xoff[k] = -1;
+#pragma unroll
+    for (int e = 0; e < PX; e++) {
+      const int qe = q + e;
+      if (gi < T::XG && qe < p.Q) {
+        const int n = qe / hw;
+        xoff[k][e] = (Off)((long long)n * chw + (long long)c * hw + (qe - n * hw));
+      } else {
+        xoff[k][e] = -1;
+      }
     }
   }
   const float *wsrc0 = p.w + (long long)m0 * p.C;
@@ -93,10 +105,20 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP,
       if (xdst[k] < 0) continue;
       float *dst = stage + xdst[k];
       const int c = xdst[k] / BP;
-      if (xoff[k] >= 0 && c < cvalid)
-        cp_async16(dst, xsrc + xoff[k]);
-      else
-        *reinterpret_cast<float4 *>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (VEC) {
+        if (xoff[k][0] >= 0 && c < cvalid)
+          cp_async16(dst, xsrc + xoff[k][0]);
+        else
+          *reinterpret_cast<float4 *>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+#pragma unroll
+        for (int e = 0; e < PX; e++) {
+          if (xoff[k][e] >= 0 && c < cvalid)
+            cp_async4(dst + e, xsrc + xoff[k][e]);
+          else
+            dst[e] = 0.0f;
+        }
+      }
     }
     float *ws = stage + BC * BP;
     const float *wsrc = wsrc0 + c0;
@@ -163,7 +185,32 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP,
   if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // epilogue: 4 consecutive pixels per (channel, group) -> one 16-byte store
+  // (VEC), or four scalar stores that may straddle two images
   float *dst = p.splits > 1 ? p.partials + (long long)split * p.part_stride : p.y;
+  if (!VEC) {
+#pragma unroll
+    for (int g = 0; g < 2; g++) {
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int q = q0 + xcol + 32 * g + e;
+        if (q >= p.Q) continue;
+        const int n = q / hw;
+        const long long base = (long long)n * p.M * hw + (q - n * hw);
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+          const int m = m0 + wrow + (r & 3) + (r >> 2) * 16;
+          if (m >= p.M) continue;
+          const float2 a = acc[r >> 1][4 * g + e];
+          dst[base + (long long)m * hw] = (r & 1) ? a.y : a.x;
+        }
+      }
+    }
+    if (p.trace && tid == 0) {
+      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      p.trace[5 * cta + 4] = global_ns();
+    }
+    return;
+  }
 #pragma unroll
   for (int g = 0; g < 2; g++) {
     const int q = q0 + xcol + 32 * g;

@@ -35,7 +35,7 @@ struct Family {
   int threads;
   const void *kernel;
   int max_ctas_per_sm;  // from __launch_bounds__
-  int kind;             // 0: conv_direct_kernel (halo staging), 1: conv1x1_vec_kernel
+  int kind;             // 0: conv_direct_kernel (halo staging), 1: conv1x1_vec_kernel, 2: its 4-byte variant
   int stages;           // cp.async pipeline depth of kind 1
 };
 
@@ -49,8 +49,15 @@ struct Family {
 #define B2C_VEC1X1(NAME, WM, WP, BC)                                                                       \
   Family {                                                                                                 \
     NAME, 1, 1, 1, Vec1x1Tile<WM, WP, BC>::BM, Vec1x1Tile<WM, WP, BC>::BP, BC, false,                      \
-        Vec1x1Tile<WM, WP, BC>::NT, reinterpret_cast<const void *>(&conv1x1_vec_kernel<WM, WP, BC>),       \
+        Vec1x1Tile<WM, WP, BC>::NT, reinterpret_cast<const void *>(&conv1x1_vec_kernel<WM, WP, BC, true>), \
         Vec1x1Tile<WM, WP, BC>::MIN_BLOCKS, 1, Vec1x1Tile<WM, WP, BC>::STAGES                              \
+  }
+// 4-byte staging variant for planes with H*W % 4 != 0 (kind 2)
+#define B2C_SCA1X1(NAME, WM, WP, BC)                                                                       \
+  Family {                                                                                                 \
+    NAME, 1, 1, 1, Vec1x1Tile<WM, WP, BC>::BM, Vec1x1Tile<WM, WP, BC>::BP, BC, false,                      \
+        Vec1x1Tile<WM, WP, BC>::NT, reinterpret_cast<const void *>(&conv1x1_vec_kernel<WM, WP, BC, false>),\
+        Vec1x1Tile<WM, WP, BC>::MIN_BLOCKS, 2, Vec1x1Tile<WM, WP, BC>::STAGES                              \
   }
 
 const Family kFamilies[] = {
@@ -77,6 +84,11 @@ const Family kFamilies[] = {
     B2C_VEC1X1("fused_1x1v_m64", 2, 4, 16),
     B2C_VEC1X1("fused_1x1v_m64p128", 2, 2, 16),
     B2C_VEC1X1("fused_1x1v_m128", 4, 2, 16),
+    // pointwise, 4-byte pixel staging (1x1, stride 1, no padding, any H*W)
+    B2C_SCA1X1("fused_1x1s_m32", 1, 4, 16),
+    B2C_SCA1X1("fused_1x1s_m64", 2, 4, 16),
+    B2C_SCA1X1("fused_1x1s_m64p128", 2, 2, 16),
+    B2C_SCA1X1("fused_1x1s_m128", 4, 2, 16),
     // paper-faithful stage 1 (strict FMUL+FADD, one filter row per blockIdx.z)
     B2C_FAMILY("stage1_strict_m32", 1, 1, 1, 32, 256, 16, true),
     B2C_FAMILY("stage1_strict_m64", 1, 1, 1, 64, 256, 16, true),
@@ -126,7 +138,7 @@ struct Candidate {
 // layers.)
 double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, int sms, int max_blocks) {
   const double fma = (double)tc.bm * tc.bp * taps * tc.bc * tc.chunks_per_split * (stage1 ? 2.0 : 1.0);
-  const double per_elem = ((long long)g.H * g.W % 4 == 0) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
+  const double per_elem = (tc.kind == 1 || ((long long)g.H * g.W % 4 == 0 && tc.kind == 0)) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
   const double loads = (per_elem * tc.tile_elems + 4.0 * tc.bm * taps) * tc.bc * tc.chunks_per_split;
   const double fixed = 250000.0 + 12.0 * tc.tile_elems;
   const double split_io = tc.splits > 1 ? (double)tc.bm * tc.bp * 24.0 : 0.0;  // partial store per CTA
@@ -162,7 +174,7 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
   base.bc = f.bc;
   base.threads = f.threads;
   base.kind = f.kind;
-  if (f.kind == 1) {
+  if (f.kind >= 1) {
     base.rs = g.W;
     base.rows = 1;
     base.tile_elems = f.bp;
@@ -279,6 +291,9 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
   if (f.strict != stage1) return false;
   if (f.kind == 1)
     return g.HF == 1 && g.WF == 1 && g.S == 1 && g.PH == 0 && g.PW == 0 && ((long long)g.H * g.W) % 4 == 0;
+  if (f.kind == 2)
+    return g.HF == 1 && g.WF == 1 && g.S == 1 && g.PH == 0 && g.PW == 0 && ((long long)g.H * g.W) % 4 != 0 &&
+           (long long)g.N * g.C * g.H * g.W < (1LL << 31);
   if (stage1) return g.S == 1;
   if (f.hf == 0) return true;  // generic
   return f.hf == g.HF && f.wf == g.WF && f.s == g.S;

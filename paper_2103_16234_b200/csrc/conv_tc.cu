@@ -148,13 +148,19 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
       const int mtiles = (int)cdiv(g.M, nf);
       const long long bstage = (long long)nf * 64 * planes;
       long long stage, smem_fixed;
-      int stages;
+      int stages, abufs = 0;
       if (mode == 1) {
         stage = (long long)tc::A_BYTES * planes + bstage;  // A + B (+ lo planes)
         smem_fixed = 0;
       } else {
-        stage = bstage;                                     // filter ring (hi + lo); A halo double-buffered
-        smem_fixed = 2 * halo * 64 * planes;
+        // filter ring (hi + lo) of `stages`; a ring of `abufs` staged halos,
+        // deep enough that ~8 taps of work are in flight (1x1 layers: many
+        // shallow channel blocks, 3x3/5x5: two suffice)
+        stage = bstage;
+        const long long abuf = halo * 64 * planes;
+        abufs = (int)std::max<long long>(2, std::min<long long>(8, cdiv(8, taps)));
+        while (abufs > 2 && abufs * abuf + 4 * stage > kSmemBudget - 2048) abufs--;
+        smem_fixed = abufs * abuf;
       }
       stages = (int)std::min<long long>(mode == 1 ? 6 : 8, (kSmemBudget - 2048 - smem_fixed) / stage);
       if (smem_fixed + 2 * stage > kSmemBudget - 2048) continue;
@@ -196,6 +202,7 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
           best.xb = mode == 1 ? xw : 0;
           best.halo = mode >= 2 ? (int)halo : 0;
           best.mh = mh;
+          best.abufs = abufs;
           best.wplanes = planes;  // filter lo plane streamed with the hi plane
           best.nf = nf;
           best.mtiles = mtiles;
@@ -207,7 +214,7 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
           best.nchunks = mode == 1 ? nchunks : 0;
           best.splits = splits;
           best.kb_per_split = kbps;
-          best.smem_bytes = (int)(stages * stage + smem_fixed) + 1024 /*align*/ + 256 /*barriers*/;
+          best.smem_bytes = (int)(stages * stage + smem_fixed) + 1024 /*align*/ + 512 /*barriers*/;
         }
       }
       if (forced_nf > 0) break;
@@ -253,6 +260,7 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   p.Wp = g.W + 2 * g.PW;
   p.halo = pl.halo;
   p.mh = pl.mh;
+  p.abufs = pl.abufs;
   p.bsplit = 0;
   if (const char *e = std::getenv("B2C_TC_BSPLIT")) p.bsplit = std::atoi(e);  // development switch
   p.C = g.C;

@@ -64,6 +64,7 @@ struct TcParams {
   int N, C, H, W, HW, S;
   int Hp, Wp, halo;  // halo variant: padded stack geometry, staged positions per tile
   int mh;            // halo variant: 128-position M halves per tile (1 or 2), sharing every filter tile
+  int abufs;         // halo variant: staged halo buffers (ring of channel blocks in flight, >= 2)
   int bsplit;        // halo variant, 3xTF32: 1 = loaders derive the filter lo plane in smem,
                      // 0 = the pre-tiled lo plane is streamed with the hi plane
   int flat;          // unpadded stride-1 1x1: chunks run over the flattened plane
@@ -328,6 +329,10 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
       const bool prof = p.dbg && blockIdx.x == 0 && leader;
       unsigned long long mt_wait = 0, mt_issue = 0;
       const unsigned long long mt_start = prof ? clock64() : 0;
+      // both operands: no-swizzle K-major core matrices, LBO 128 B (K), SBO 512 B (rows)
+      const uint64_t a_desc0 = umma_desc(smem_base, 128, 512, LAYOUT_NONE);
+      const uint32_t idesc = p.idesc;
+      const uint32_t nf = (uint32_t)p.NF;
       for (int kb = 0; kb < KB; kb++) {
         const int s = kb % S;
         const uint32_t ph = (kb / S) & 1;
@@ -336,24 +341,20 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
         mbar_wait(ready_bar(s), ph, p.spin_limit, p.dbg, 0x280000u | kb);
         tc_fence_after();
         if (prof) { const unsigned long long c = clock64(); mt_wait += c - c0; c0 = c; }
-        const uint32_t sa = smem_base + (uint32_t)s * p.stage_bytes;
-        const uint32_t sb = sa + b_off;
+        // descriptors advanced by adding 16-byte units to the start-address field
+        const uint64_t a0 = a_desc0 + (((uint32_t)s * p.stage_bytes) >> 4);
+        const uint64_t b0 = a0 + (b_off >> 4);
+        if (leader && !(p.mode & 2)) {
 #pragma unroll
-        for (int k = 0; k < BC / 8; k++) {
-          if (p.mode & 2) continue;
-          const uint64_t a_hi = umma_desc(sa + k * 256, 128, 512, LAYOUT_NONE);
-          const uint64_t b_hi = umma_desc(sb + k * 256, 128, 512, LAYOUT_NONE);
-          const uint64_t a_lo = umma_desc(sa + A_TILE + k * 256, 128, 512, LAYOUT_NONE);
-          const uint64_t b_lo = umma_desc(sb + b_plane + k * 256, 128, 512, LAYOUT_NONE);
-          if (leader) {
-            umma_tf32(tmem_d, a_hi, b_hi, p.idesc, (kb | k) != 0);
+          for (int k = 0; k < BC / 8; k++) {
+            const uint32_t acc = (kb | k) != 0;
+            umma_tf32(tmem_d, a0 + k * 16, b0 + k * 16, idesc, acc);
             if (PASSES == 3) {  // correction terms into their own accumulator (columns NF..2NF):
               // the main accumulator then sees a third of the accumulation steps
-              umma_tf32(tmem_d + p.NF, a_hi, b_lo, p.idesc, (kb | k) != 0);
-              umma_tf32(tmem_d + p.NF, a_lo, b_hi, p.idesc, 1);
+              umma_tf32(tmem_d + nf, a0 + k * 16, b0 + (b_plane >> 4) + k * 16, idesc, acc);
+              umma_tf32(tmem_d + nf, a0 + (A_TILE >> 4) + k * 16, b0 + k * 16, idesc, 1);
             }
           }
-          __syncwarp();
         }
         if (leader) umma_commit(empty_bar(s));  // frees the stage once these MMAs have read it
         __syncwarp();
@@ -533,11 +534,12 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
   const uint32_t a_buf = a_bytes * (PASSES == 3 ? 2u : 1u);
   const uint32_t b_plane = (uint32_t)p.NF * BC * 4;  // one filter plane (hi or lo)
   const uint32_t b_stage = b_plane * (PASSES == 3 ? 2u : 1u);
-  uint8_t *bring = smem + 2 * a_buf;
+  const int SA = p.abufs;                            // halo ring depth (channel blocks in flight)
+  uint8_t *bring = smem + (size_t)SA * a_buf;
   uint64_t *bars = reinterpret_cast<uint64_t *>(bring + (size_t)S * b_stage);
   // bars: [0,S) b_full (hi landed), [S,2S) b_ready (lo split), [2S,3S) b_empty,
-  //       3S+{0,1} a_full, 3S+{2,3} a_empty, 3S+4 accum
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 5);
+  //       [3S, 3S+SA) a_full, [3S+SA, 3S+2SA) a_empty, 3S+2SA accum
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 2 * SA + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -556,8 +558,8 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
   auto b_ready = [&](int s) { return bar_base + 8u * (S + s); };
   auto b_empty = [&](int s) { return bar_base + 8u * (2 * S + s); };
   auto a_full = [&](int b) { return bar_base + 8u * (3 * S + b); };
-  auto a_empty = [&](int b) { return bar_base + 8u * (3 * S + 2 + b); };
-  const uint32_t accum_bar = bar_base + 8u * (3 * S + 4);
+  auto a_empty = [&](int b) { return bar_base + 8u * (3 * S + SA + b); };
+  const uint32_t accum_bar = bar_base + 8u * (3 * S + 2 * SA);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
@@ -565,7 +567,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
       mbar_init(b_ready(s), LOADERS / 32);
       mbar_init(b_empty(s), 1);
     }
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < SA; b++) {
       mbar_init(a_full(b), LOADERS / 32);
       mbar_init(a_empty(b), 1);
     }
@@ -628,9 +630,9 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
       const uint32_t nf = (uint32_t)p.NF;
       const int taps = p.taps, wf = p.WF, wp = p.Wp;
       for (int i = 0; i < NCB; i++) {
-        const int buf = i & 1;
+        const int buf = i % SA;
         unsigned long long c0 = prof ? clock64() : 0;
-        mbar_wait(a_full(buf), (i >> 1) & 1, p.spin_limit, p.dbg, 0x210000u | i);
+        mbar_wait(a_full(buf), (i / SA) & 1, p.spin_limit, p.dbg, 0x210000u | i);
         if (prof) mt_wait_a += clock64() - c0;
         tc_fence_after();
         const uint64_t a_buf_desc = a_desc0 + ((buf * a_buf) >> 4);
@@ -693,10 +695,10 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
     unsigned long long lt_wait = 0, lt_fill = 0;
     const unsigned long long lt_start = prof ? clock64() : 0;
     for (int i = 0; i < NCB; i++) {
-      const int buf = i & 1;
+      const int buf = i % SA;
       unsigned long long c0 = prof ? clock64() : 0;
-      if (i >= 2) {
-        if (lane == 0) mbar_wait(a_empty(buf), ((i >> 1) - 1) & 1, p.spin_limit, p.dbg, 0x310000u | i);
+      if (i >= SA) {
+        if (lane == 0) mbar_wait(a_empty(buf), ((i / SA) - 1) & 1, p.spin_limit, p.dbg, 0x310000u | i);
         __syncwarp();
       }
       if (prof) { const unsigned long long c = clock64(); lt_wait += c - c0; c0 = c; }

@@ -32,6 +32,7 @@ struct TcPlan {
   int xb = 0;        // gather mode: chunk width XW in output columns (32, 16 or 8; chunk = 32/XW rows)
   int halo = 0;      // halo mode (stride 1): staged positions per tile (0 = gather mode)
   int mh = 1;        // halo mode: 128-position M halves per tile
+  int abufs = 0;     // halo mode: staged halo buffers (ring depth)
   int wplanes = 1;   // pre-tiled filter planes streamed from HBM/L2 (gather 3xTF32: hi + lo)
   int nf = 0;        // output channels per tile (UMMA N)
   int mtiles = 0;
