@@ -62,6 +62,9 @@ def parse():
                     help="tensor-core variant reported separately in the same line (north star: optional, own tolerance)")
     ap.add_argument("--report", default="", help="write a per-layer sweep of every BASELINE config to PATH")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--schedule", choices=("dataflow", "sequential"), default="dataflow",
+                    help="dataflow: data-independent layers of the source network (inception branches, ResNet "
+                         "projection shortcuts) run concurrently inside the step graph; sequential: one stream")
     ap.add_argument("--e2e-steps", type=int, default=3)
     return ap.parse_args()
 
@@ -270,16 +273,38 @@ def sweep_report(path, device, peak_tflops):
     return rows
 
 
-def time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank):
+def time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank, groups=None):
     """Warm up, capture one step (every layer once) as a CUDA graph, then time
     exactly `steps` replays between barriers + synchronize (CUDA events on
-    the replay stream, max over ranks).  Returns (ms, launches/step, clocks)."""
+    the replay stream, max over ranks).  `groups` (workloads.schedule) runs
+    data-independent layers of a group on parallel streams inside the graph
+    (fork/join by events); groups in order.  Returns (ms, launches/step, clocks)."""
     import torch
     import torch.distributed as dist
 
+    groups = groups or [[i] for i in range(len(layers))]
+    side = [torch.cuda.Stream() for _ in range(max(len(g) for g in groups))]
+
     def step():
-        for L, x, w, y in zip(layers, xs, ws, ys):
-            L(x, w, out=y)
+        main = torch.cuda.current_stream()
+        for grp in groups:
+            if len(grp) == 1:
+                i = grp[0]
+                layers[i](xs[i], ws[i], out=ys[i])
+                continue
+            fork = torch.cuda.Event()
+            fork.record(main)
+            joins = []
+            for k, i in enumerate(grp):
+                s = side[k]
+                s.wait_event(fork)
+                with torch.cuda.stream(s):
+                    layers[i](xs[i], ws[i], out=ys[i])
+                ev = torch.cuda.Event()
+                ev.record(s)
+                joins.append(ev)
+            for ev in joins:
+                main.wait_event(ev)
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -377,7 +402,10 @@ def tensor_core_variant(args, lib, nat, cfgs, xs, ws, ys, world, device, local_r
 
     eng = args.tc_engine
     layers = [ConvLayer(c, eng) for c in cfgs]
-    ms_total, launches, clk = time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank)
+    from paper_2103_16234_b200 import workloads as W
+
+    groups = W.schedule(args.workload, cfgs) if args.schedule == "dataflow" else None
+    ms_total, launches, clk = time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank, groups)
     flops = sum(c.flops for c in cfgs)
     layer_ms = time_layers(layers, xs, ws, ys)
     kern_ms = sum(layer_ms)
@@ -420,6 +448,8 @@ def main():
     config = {"workload": f"{args.workload}: {W.DESCRIPTIONS[args.workload]}", "layers": len(cfgs),
               "global_batch": global_batch, "batch_per_gpu": per_rank, "engine": args.engine,
               "parallelism": f"batch-sharded dp{world} (filters replicated, no collective)",
+              "schedule": args.schedule + (" (inception branches / projection shortcuts concurrent, "
+                                           "modules and blocks in order)" if args.schedule == "dataflow" else ""),
               "l2": "per-step working set > 126 MB L2 (each layer's operands evicted by the others between steps)"}
 
     if args.impl == "reference":
@@ -444,7 +474,8 @@ def main():
 
     layers = [ConvLayer(c, args.engine) for c in cfgs]
     xs, ws, ys = make_operands(cfgs, device, 1234 + rank)
-    ms_total, launches_per_step, clk = time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank)
+    groups = W.schedule(args.workload, cfgs) if args.schedule == "dataflow" else None
+    ms_total, launches_per_step, clk = time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank, groups)
     flops_step_rank = sum(c.flops for c in cfgs)
     value = flops_step_rank * world * args.steps / (ms_total * 1e-3) / 1e9
     ms_per_step = ms_total / args.steps

@@ -80,3 +80,35 @@ def layers(workload: str, n: int) -> list[ConvConfig]:
     table, _ = WORKLOADS[workload]
     return [ConvConfig(name, n=n, c=c, h=h, w=h, m=m, hf=f, wf=f, stride=s, pad_h=p, pad_w=p)
             for name, c, h, m, f, s, p in table]
+
+
+def schedule(workload: str, cfgs: list[ConvConfig]) -> list[list[int]]:
+    """Dataflow order of a workload's layers for one inference step: groups of
+    layer indices that are data-independent in the source network and may
+    run concurrently, the groups in dependency order.
+
+    C2  the four branch convolutions of a GoogLeNet inception module (1x1,
+        3x3reduce, 5x5reduce read the module input; poolproj reads its
+        3x3/s1 max-pool) are independent; modules are sequential.
+    C5  in the first block of each ResNet stage the projection shortcut
+        (downsample) and conv1 both read the block input; all else chains.
+    C1, C3, C4  sequential (single layer; layers of different modules; VGG).
+    """
+    if workload == "c2":
+        groups: dict[str, list[int]] = {}
+        for i, c in enumerate(cfgs):
+            groups.setdefault(c.name.split("-")[0], []).append(i)
+        return list(groups.values())
+    if workload == "c5":
+        out, idx = [], {c.name: i for i, c in enumerate(cfgs)}
+        for i, c in enumerate(cfgs):
+            if c.name.endswith(".downsample"):
+                continue
+            grp = [i]
+            if c.name.endswith(".conv1"):
+                ds = c.name[: -len("conv1")] + "downsample"
+                if ds in idx:
+                    grp.append(idx[ds])
+            out.append(grp)
+        return out
+    return [[i] for i in range(len(cfgs))]
