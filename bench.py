@@ -237,6 +237,33 @@ def time_layers(layers, xs, ws, ys, reps=20):
     return out
 
 
+def time_cudnn(cfgs, xs, ws, reps=10):
+    """cuDNN fp32 (TF32 disabled) through torch, per layer, best algorithm
+    (benchmark mode) -- an external library baseline for the report only (the
+    paper compares cuConv against the best cuDNN algorithm)."""
+    import torch
+    import torch.nn.functional as F
+
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.benchmark = True
+    out = []
+    for c, x, w in zip(cfgs, xs, ws):
+        def run():
+            return F.conv2d(x, w, stride=c.stride, padding=(c.pad_h, c.pad_w))
+        for _ in range(3):
+            run()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            run()
+        b.record()
+        b.synchronize()
+        out.append(a.elapsed_time(b) / reps)
+    torch.backends.cudnn.benchmark = False
+    return out
+
+
 def sweep_report(path, device, peak_tflops):
     """Per-layer µs / GFLOP/s / roofline for every BASELINE config and batch."""
     import torch
@@ -253,7 +280,8 @@ def sweep_report(path, device, peak_tflops):
             ms = time_layers(layers, xs, ws, ys, reps=10)
             tcl = [ConvLayer(c, "tf32x3") for c in cfgs]
             tms = time_layers(tcl, xs, ws, ys, reps=10)
-            for c, L, t, T, tt in zip(cfgs, layers, ms, tcl, tms):
+            cud = time_cudnn(cfgs, xs, ws, reps=10)
+            for c, L, t, T, tt, cu in zip(cfgs, layers, ms, tcl, tms, cud):
                 flop_per_byte = c.flops / c.compulsory_bytes
                 ridge = peak_tflops * 1e12 / (hbm * 1e9)
                 if flop_per_byte >= ridge:
@@ -265,7 +293,9 @@ def sweep_report(path, device, peak_tflops):
                              "gflops": round(c.flops / (t * 1e-3) / 1e9, 1), "bound": bound,
                              "roofline_frac": round(frac, 4), "family": L.family, "grid": L.grid,
                              "tf32x3_us": round(tt * 1e3, 2), "tf32x3_gflops": round(c.flops / (tt * 1e-3) / 1e9, 1),
-                             "tf32x3_plan": T.family})
+                             "tf32x3_plan": T.family,
+                             "cudnn_fp32_us": round(cu * 1e3, 2),
+                             "cudnn_fp32_gflops": round(c.flops / (cu * 1e-3) / 1e9, 1)})
             del xs, ws, ys
             torch.cuda.empty_cache()
     with open(path, "w") as fh:

@@ -132,6 +132,8 @@ typedef struct {
   int32_t halo_positions;   /* out: staged positions per tile (mode 2)        */
   int32_t m_halves;         /* out: 128-pixel UMMA M halves per tile (mode 2:
                                1 or 2, sharing each filter tile)              */
+  int32_t bf16_corrections; /* out: 3xTF32 correction products run as bf16
+                               MMAs (K=16, twice the tf32 rate; mode 2)       */
 } b2c_tc_plan;
 
 /* ---------------------------------------------------------------- metadata */

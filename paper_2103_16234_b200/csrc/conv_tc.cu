@@ -25,8 +25,10 @@ const void *tc_kernel(int passes, bool halo, int mh) {
   if (halo) {
     if (mh == 2)
       return passes == 3 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<3, 2>)
+           : passes == 2 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<2, 2>)
                          : reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<1, 2>);
     return passes == 3 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<3, 1>)
+         : passes == 2 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<2, 1>)
                        : reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<1, 1>);
   }
   return passes == 3 ? reinterpret_cast<const void *>(&tc::conv_tc_kernel<3>)
@@ -36,6 +38,15 @@ const void *tc_kernel(int passes, bool halo, int mh) {
 constexpr int kSmemBudget = 225 * 1024;  // dynamic smem per CTA incl. 1 KB alignment slack + barriers
 
 }  // namespace
+
+// 3xTF32 correction products as bf16 MMAs (halo mode).  Default on; B2C_TC_BF16CORR=0 disables.
+bool bf16corr_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("B2C_TC_BF16CORR");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
 
 bool tc_flat(const Geom &g) { return g.HF == 1 && g.WF == 1 && g.S == 1 && g.PH == 0 && g.PW == 0; }
 
@@ -182,7 +193,10 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
         // 128x256x8 tf32 UMMA; gather mode adds a ~1.1-1.3k clk latency chain
         // per k-block, halo mode ~150 clk of barrier work per tap and one
         // double-buffered halo fill per channel block
-        const double mma = passes * 2.0 * mh * std::max(95.0 * nf / 256.0, 12.0);
+        const bool bf16corr = passes == 3 && mode >= 2 && bf16corr_enabled();
+        // tf32 MMA-equivalents per k-block and M half: 2 (main) [+ 4 tf32 or 2 bf16 corrections]
+        const double mma_units = passes == 1 ? 2.0 : (bf16corr ? 4.0 : 6.0);
+        const double mma = mma_units * mh * std::max(95.0 * nf / 256.0, 12.0);
         double t_cta;
         if (mode == 1) {
           t_cta = kbps * std::max(mma, passes == 3 ? 1300.0 : 1100.0);
@@ -204,6 +218,7 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
           best.mh = mh;
           best.abufs = abufs;
           best.wplanes = planes;  // filter lo plane streamed with the hi plane
+          best.bf16corr = bf16corr;
           best.nf = nf;
           best.mtiles = mtiles;
           best.stages = stages;
@@ -238,11 +253,20 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   float *wt = static_cast<float *>(workspace);
   const int planes = (pl.halo > 0 && pl.passes == 3 && std::getenv("B2C_TC_BSPLIT") && std::atoi(std::getenv("B2C_TC_BSPLIT")))
                          ? 1 : pl.wplanes;
-  {
+  // 3xTF32 in halo mode: correction products as bf16 MMAs (kernel PASSES 2) when the plan says so
+  const int kpasses = (pl.passes == 3 && pl.halo > 0 && pl.bf16corr) ? 2 : pl.passes;
+  if (kpasses == 2) {
+    const long long total = (long long)cblocks * taps * Mp * tc::BC;
+    const int blocks = (int)std::min<long long>(cdiv(total, 256), 8LL * device_sm_count(0));
+    note_launch();
+    tc::filter_tile_bf16corr_kernel<<<blocks, 256, 0, stream>>>(w, wt, g.M, g.C, taps, pl.nf, pl.mtiles, cblocks);
+  } else {
     const long long total = (long long)cblocks * taps * Mp * tc::BC * planes;
     const int blocks = (int)std::min<long long>(cdiv(total, 256), 8LL * device_sm_count(0));
     note_launch();
     tc::filter_tile_kernel<<<blocks, 256, 0, stream>>>(w, wt, g.M, g.C, taps, pl.nf, pl.mtiles, cblocks, planes);
+  }
+  {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -301,7 +325,7 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   p.spin_limit = 4000000000ull;  // 4 s
   if (const char *m = std::getenv("B2C_TC_MODE")) p.mode = std::atoi(m);
 
-  const void *kern = tc_kernel(pl.passes, pl.halo > 0, pl.mh);
+  const void *kern = tc_kernel(kpasses, pl.halo > 0, pl.mh);
   static std::mutex mu;
   {
     std::lock_guard<std::mutex> lk(mu);

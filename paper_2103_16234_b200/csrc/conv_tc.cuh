@@ -46,6 +46,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -156,7 +157,17 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
-__device__ __forceinline__ float tf32_lo(float a) { return a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u); }
+__device__ __forceinline__ float tf32_hi(float a) { return __uint_as_float(__float_as_uint(a) & 0xFFFFE000u); }
+__device__ __forceinline__ float tf32_lo(float a) { return a - tf32_hi(a); }
+// two floats -> packed bf16x2 (round to nearest even), low half = first
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
 
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1, int c2,
                                             int c3) {
@@ -199,6 +210,14 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
@@ -531,9 +550,11 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
   const int TP = TILE_P * MH;                        // output positions per tile
   const uint32_t a_plane = (uint32_t)p.halo * 16u;   // bytes of one 4-channel K-core plane
   const uint32_t a_bytes = a_plane * 4u;             // one A plane (hi or lo): 16 channels
-  const uint32_t a_buf = a_bytes * (PASSES == 3 ? 2u : 1u);
-  const uint32_t b_plane = (uint32_t)p.NF * BC * 4;  // one filter plane (hi or lo)
-  const uint32_t b_stage = b_plane * (PASSES == 3 ? 2u : 1u);
+  // PASSES 3: fp32 hi + fp32 lo planes; PASSES 2: fp32 hi + bf16(hi) + bf16(lo)
+  // planes (the correction products run as bf16 MMAs, K=16 at twice the rate)
+  const uint32_t a_buf = a_bytes * (PASSES >= 2 ? 2u : 1u);
+  const uint32_t b_plane = (uint32_t)p.NF * BC * 4;  // one fp32 filter plane
+  const uint32_t b_stage = b_plane * (PASSES >= 2 ? 2u : 1u);
   const int SA = p.abufs;                            // halo ring depth (channel blocks in flight)
   uint8_t *bring = smem + (size_t)SA * a_buf;
   uint64_t *bars = reinterpret_cast<uint64_t *>(bring + (size_t)S * b_stage);
@@ -600,7 +621,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
         const unsigned long long c0 = prof ? clock64() : 0;
         if (kb >= S) mbar_wait(b_empty(s), ((kb / S) - 1) & 1, p.spin_limit, p.dbg, 0x110000u | kb);
         if (prof) qt_wait += clock64() - c0;
-        const uint32_t bytes = (PASSES == 3 && !p.bsplit) ? b_stage : b_plane;
+        const uint32_t bytes = (PASSES >= 2 && !(PASSES == 3 && p.bsplit)) ? b_stage : b_plane;
         const float *src = p.wt + ((long long)(cb_base * p.taps + kb) * p.mtiles + mt) * (bytes / 4);
         if (leader) {
           if (p.mode & 8) {
@@ -626,6 +647,12 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
       const unsigned long long mt_start = prof ? clock64() : 0;
       const uint64_t a_desc0 = umma_desc(smem_base, a_plane, 128, LAYOUT_NONE);
       const uint64_t b_desc0 = umma_desc(bring_base, 128, 512, LAYOUT_NONE);
+      // bf16 planes: K-cores of 8 channels; A rows stay 16 B per position (LBO = halo*16),
+      // B: LBO 128 B (next 8 channels), SBO 256 B (next 8 filters)
+      const uint64_t a16_desc0 = umma_desc(smem_base, a_plane, 128, LAYOUT_NONE);
+      const uint64_t b16_delta = umma_desc(0, 128, 256, LAYOUT_NONE) - umma_desc(0, 128, 512, LAYOUT_NONE);
+      const uint32_t idesc16 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.NF >> 3) << 17) | (8u << 24);
+      (void)a16_desc0;
       const uint32_t idesc = p.idesc;
       const uint32_t nf = (uint32_t)p.NF;
       const int taps = p.taps, wf = p.WF, wp = p.Wp;
@@ -659,6 +686,23 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
 #pragma unroll
               for (int h = 0; h < MH; h++)
                 if (!(p.mode & 2)) umma_tf32(tmem_d + h * nf, ak + h * (TILE_P * 16 >> 4), bh, idesc, acc);
+              if (PASSES == 2 && k == 0) {
+                // bf16 corrections over the whole 16-channel block (one K=16 MMA each)
+                const uint32_t acc16 = kb != 0;
+                const uint64_t bh16 = b0 + (b_plane >> 4) + b16_delta, bl16 = bh16 + (uint64_t)(nf * 32 >> 4);
+#pragma unroll
+                for (int h = 0; h < MH; h++) {
+                  const uint64_t ah16 = a0 + (a_bytes >> 4) + h * (TILE_P * 16 >> 4);
+                  if (!(p.mode & 2)) {
+                    umma_f16(tmem_d + (MH + h) * nf, ah16, bl16, idesc16, acc16);
+                  }
+                }
+#pragma unroll
+                for (int h = 0; h < MH; h++) {
+                  const uint64_t al16 = a0 + ((a_bytes + a_bytes / 2) >> 4) + h * (TILE_P * 16 >> 4);
+                  if (!(p.mode & 2)) umma_f16(tmem_d + (MH + h) * nf, al16, bh16, idesc16, 1);
+                }
+              }
               if (PASSES == 3) {
 #pragma unroll
                 for (int h = 0; h < MH; h++)
@@ -723,6 +767,11 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
         sts128(dst, make_float4(v[0], v[1], v[2], v[3]));
         if (PASSES == 3)
           sts128(dst + a_bytes, make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3])));
+        if (PASSES == 2) {  // bf16(hi), bf16(lo): K-core j/2 (8 channels), 8-byte half-row (j%2)
+          const uint32_t d16 = sa + a_bytes + (uint32_t)(j >> 1) * a_plane + (uint32_t)pos * 16u + (j & 1) * 8u;
+          sts64(d16, pack_bf16(tf32_hi(v[0]), tf32_hi(v[1])), pack_bf16(tf32_hi(v[2]), tf32_hi(v[3])));
+          sts64(d16 + a_bytes / 2, pack_bf16(tf32_lo(v[0]), tf32_lo(v[1])), pack_bf16(tf32_lo(v[2]), tf32_lo(v[3])));
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -770,7 +819,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
       for (int j0 = colgrp * 32; j0 < p.NF; j0 += 32 * COLGRPS) {
         uint32_t rr[32];
         tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + h * p.NF + j0, rr);
-        if (PASSES == 3) {
+        if (PASSES >= 2) {
           uint32_t c[32];
           tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + (MH + h) * p.NF + j0, c);
 #pragma unroll
@@ -823,6 +872,37 @@ __global__ void __launch_bounds__(256) filter_tile_kernel(const float *__restric
     const int c = cb * BC + j * 4 + e;
     const float v = (m < M && c < C) ? w[((long long)m * C + c) * taps + t] : 0.0f;
     wt[i] = plane == 0 ? v : tf32_lo(v);
+  }
+}
+
+// Filter tiles for the bf16-correction 3xTF32 variant (PASSES 2): per
+// (cb, tap, filter tile) block, the fp32 plane (as filter_tile_kernel) then
+// bf16(hi) and bf16(lo) planes in bf16 K-major core-matrix order (8 filters x
+// 8 channels = 128 B per core matrix; K-adjacent 128 B apart, 8-filter groups
+// 256 B apart).
+__global__ void __launch_bounds__(256) filter_tile_bf16corr_kernel(const float *__restrict__ w, float *__restrict__ wt,
+                                                                   int M, int C, int taps, int NF, int mtiles,
+                                                                   int cblocks) {
+  const long long tile = (long long)NF * BC;  // elements of one block
+  const long long total = (long long)cblocks * taps * mtiles * tile;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long blk = i / tile;  // (cb, tap, filter tile)
+    const int within = (int)(i - blk * tile);
+    const int mt = (int)(blk % mtiles);
+    const long long kb = blk / mtiles;
+    const int t = (int)(kb % taps);
+    const int cb = (int)(kb / taps);
+    const int ml = within / BC, cl = within - (within / BC) * BC;  // local filter row, channel
+    const int m = mt * NF + ml;
+    const int c = cb * BC + cl;
+    const float v = (m < M && c < C) ? w[((long long)m * C + c) * taps + t] : 0.0f;
+    float *base = wt + blk * 2 * tile;  // 2 fp32-plane equivalents per block
+    // fp32 plane: core (g = ml/8, j = cl/4), row ml%8, element cl%4
+    base[(ml >> 3) * 128 + (cl >> 2) * 32 + (ml & 7) * 4 + (cl & 3)] = v;
+    __nv_bfloat16 *b16 = reinterpret_cast<__nv_bfloat16 *>(base + tile);
+    const int o16 = (ml >> 3) * 128 + (cl >> 3) * 64 + (ml & 7) * 8 + (cl & 7);  // in bf16 elements
+    b16[o16] = __float2bfloat16_rn(tf32_hi(v));
+    b16[NF * BC + o16] = __float2bfloat16_rn(tf32_lo(v));
   }
 }
 
