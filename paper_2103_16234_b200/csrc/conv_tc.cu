@@ -22,6 +22,7 @@ namespace {
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 
 const void *tc_kernel(int passes, bool halo, int mh) {
+  if (!halo && passes == 2) return reinterpret_cast<const void *>(&tc::conv_tc_kernel<2>);
   if (halo) {
     if (mh == 2)
       return passes == 3 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<3, 2>)
@@ -193,7 +194,7 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
         // 128x256x8 tf32 UMMA; gather mode adds a ~1.1-1.3k clk latency chain
         // per k-block, halo mode ~150 clk of barrier work per tap and one
         // double-buffered halo fill per channel block
-        const bool bf16corr = passes == 3 && mode >= 2 && bf16corr_enabled();
+        const bool bf16corr = passes == 3 && bf16corr_enabled();
         // tf32 MMA-equivalents per k-block and M half: 2 (main) [+ 4 tf32 or 2 bf16 corrections]
         const double mma_units = passes == 1 ? 2.0 : (bf16corr ? 4.0 : 6.0);
         const double mma = mma_units * mh * std::max(95.0 * nf / 256.0, 12.0);
@@ -254,7 +255,7 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   const int planes = (pl.halo > 0 && pl.passes == 3 && std::getenv("B2C_TC_BSPLIT") && std::atoi(std::getenv("B2C_TC_BSPLIT")))
                          ? 1 : pl.wplanes;
   // 3xTF32 in halo mode: correction products as bf16 MMAs (kernel PASSES 2) when the plan says so
-  const int kpasses = (pl.passes == 3 && pl.halo > 0 && pl.bf16corr) ? 2 : pl.passes;
+  const int kpasses = (pl.passes == 3 && pl.bf16corr) ? 2 : pl.passes;
   if (kpasses == 2) {
     const long long total = (long long)cblocks * taps * Mp * tc::BC;
     const int blocks = (int)std::min<long long>(cdiv(total, 256), 8LL * device_sm_count(0));

@@ -165,6 +165,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+__device__ __forceinline__ void sts128u(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 __device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
   asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
@@ -290,7 +293,9 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
   // stage layout: [A hi | A lo (3xTF32) | B hi | B lo (3xTF32)], every operand in
   // no-swizzle K-major core matrices (8 rows x 16 B; K-adjacent 128 B apart,
   // 8-row groups 512 B apart)
-  const uint32_t b_off = A_TILE * (PASSES == 3 ? 2 : 1);
+  // PASSES 3: [A hi | A lo | B hi | B lo] fp32 planes; PASSES 2: [A fp32 | A bf16(hi) |
+  // A bf16(lo) | B fp32 | B bf16(hi) | B bf16(lo)] (corrections as bf16 MMAs)
+  const uint32_t b_off = A_TILE * (PASSES >= 2 ? 2 : 1);
   const uint32_t b_plane = (uint32_t)p.NF * BC * 4;
 
   if (threadIdx.x == 0) {
@@ -352,6 +357,9 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
       const uint64_t a_desc0 = umma_desc(smem_base, 128, 512, LAYOUT_NONE);
       const uint32_t idesc = p.idesc;
       const uint32_t nf = (uint32_t)p.NF;
+      // bf16 planes: core matrices of 8 rows x 8 channels, SBO 256 B instead of 512 B
+      const uint64_t sbo_delta = umma_desc(0, 128, 256, LAYOUT_NONE) - umma_desc(0, 128, 512, LAYOUT_NONE);
+      const uint32_t idesc16 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.NF >> 3) << 17) | (8u << 24);
       for (int kb = 0; kb < KB; kb++) {
         const int s = kb % S;
         const uint32_t ph = (kb / S) & 1;
@@ -373,6 +381,12 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
               umma_tf32(tmem_d + nf, a0 + k * 16, b0 + (b_plane >> 4) + k * 16, idesc, acc);
               umma_tf32(tmem_d + nf, a0 + (A_TILE >> 4) + k * 16, b0 + k * 16, idesc, 1);
             }
+          }
+          if (PASSES == 2) {  // bf16 corrections, one K=16 MMA each: bf16(a_hi)*bf16(b_lo) + bf16(a_lo)*bf16(b_hi)
+            const uint64_t a16 = a0 + (A_TILE >> 4) + sbo_delta;
+            const uint64_t b16 = b0 + (b_plane >> 4) + sbo_delta;
+            umma_f16(tmem_d + nf, a16, b16 + (uint64_t)(nf * 32 >> 4), idesc16, kb != 0);
+            umma_f16(tmem_d + nf, a16 + (A_TILE / 2 >> 4), b16, idesc16, 1);
           }
         }
         if (leader) umma_commit(empty_bar(s));  // frees the stage once these MMAs have read it
@@ -449,6 +463,14 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
           sts128(st + A_TILE, make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3])));
           sts128(st + A_TILE + 128, make_float4(tf32_lo(v[4]), tf32_lo(v[5]), tf32_lo(v[6]), tf32_lo(v[7])));
         }
+        if (PASSES == 2) {  // this thread's 8 channels are one bf16 core-matrix row (16 B)
+          const uint32_t d16 = smem_base + (uint32_t)s * p.stage_bytes + A_TILE + (uint32_t)((pix >> 3) * 256 +
+                               cgrp * 128 + (pix & 7) * 16);
+          sts128u(d16, pack_bf16(tf32_hi(v[0]), tf32_hi(v[1])), pack_bf16(tf32_hi(v[2]), tf32_hi(v[3])),
+                  pack_bf16(tf32_hi(v[4]), tf32_hi(v[5])), pack_bf16(tf32_hi(v[6]), tf32_hi(v[7])));
+          sts128u(d16 + A_TILE / 2, pack_bf16(tf32_lo(v[0]), tf32_lo(v[1])), pack_bf16(tf32_lo(v[2]), tf32_lo(v[3])),
+                  pack_bf16(tf32_lo(v[4]), tf32_lo(v[5])), pack_bf16(tf32_lo(v[6]), tf32_lo(v[7])));
+        }
       }
       if (prof) { const unsigned long long c = clock64(); pt_store += c - c0; c0 = c; }
       // generic-proxy smem writes -> visible to the tensor core (async proxy);
@@ -505,7 +527,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
     for (int j0 = colgrp * 32; j0 < p.NF; j0 += 32 * COLGRPS) {
       uint32_t r[32];
       tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + j0, r);
-      if (PASSES == 3) {  // main + correction accumulator, fp32 round-to-nearest
+      if (PASSES >= 2) {  // main + correction accumulator, fp32 round-to-nearest
         uint32_t c[32];
         tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + p.NF + j0, c);
 #pragma unroll
