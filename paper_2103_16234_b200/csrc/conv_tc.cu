@@ -252,8 +252,7 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   const int Mp = pl.mtiles * pl.nf;
   if (!workspace || ws_bytes < tc_workspace_bytes(g, pl)) return cudaErrorInvalidValue;
   float *wt = static_cast<float *>(workspace);
-  const int planes = (pl.halo > 0 && pl.passes == 3 && std::getenv("B2C_TC_BSPLIT") && std::atoi(std::getenv("B2C_TC_BSPLIT")))
-                         ? 1 : pl.wplanes;
+  const int planes = pl.wplanes;
   // 3xTF32 in halo mode: correction products as bf16 MMAs (kernel PASSES 2) when the plan says so
   const int kpasses = (pl.passes == 3 && pl.bf16corr) ? 2 : pl.passes;
   if (kpasses == 2) {
@@ -286,8 +285,6 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   p.halo = pl.halo;
   p.mh = pl.mh;
   p.abufs = pl.abufs;
-  p.bsplit = 0;
-  if (const char *e = std::getenv("B2C_TC_BSPLIT")) p.bsplit = std::atoi(e);  // development switch
   p.C = g.C;
   p.H = g.H;
   p.W = g.W;

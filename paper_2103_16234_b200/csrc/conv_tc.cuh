@@ -66,8 +66,6 @@ struct TcParams {
   int Hp, Wp, halo;  // halo variant: padded stack geometry, staged positions per tile
   int mh;            // halo variant: 128-position M halves per tile (1 or 2), sharing every filter tile
   int abufs;         // halo variant: staged halo buffers (ring of channel blocks in flight, >= 2)
-  int bsplit;        // halo variant, 3xTF32: 1 = loaders derive the filter lo plane in smem,
-                     // 0 = the pre-tiled lo plane is streamed with the hi plane
   int flat;          // unpadded stride-1 1x1: chunks run over the flattened plane
   int M, Wo, HoWo;   // output geometry (Wo = HoWo for flattened 1x1)
   int Ho;            // output rows (1 for flattened)
@@ -580,7 +578,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
   const int SA = p.abufs;                            // halo ring depth (channel blocks in flight)
   uint8_t *bring = smem + (size_t)SA * a_buf;
   uint64_t *bars = reinterpret_cast<uint64_t *>(bring + (size_t)S * b_stage);
-  // bars: [0,S) b_full (hi landed), [S,2S) b_ready (lo split), [2S,3S) b_empty,
+  // bars: [0,S) b_full (filter planes landed), [S,2S) unused, [2S,3S) b_empty,
   //       [3S, 3S+SA) a_full, [3S+SA, 3S+2SA) a_empty, 3S+2SA accum
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 2 * SA + 1);
 
@@ -598,7 +596,6 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
   const uint32_t bring_base = smem_u32(bring);
   const uint32_t bar_base = smem_u32(bars);
   auto b_full = [&](int s) { return bar_base + 8u * s; };
-  auto b_ready = [&](int s) { return bar_base + 8u * (S + s); };
   auto b_empty = [&](int s) { return bar_base + 8u * (2 * S + s); };
   auto a_full = [&](int b) { return bar_base + 8u * (3 * S + b); };
   auto a_empty = [&](int b) { return bar_base + 8u * (3 * S + SA + b); };
@@ -607,7 +604,6 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
       mbar_init(b_full(s), 1);
-      mbar_init(b_ready(s), LOADERS / 32);
       mbar_init(b_empty(s), 1);
     }
     for (int b = 0; b < SA; b++) {
@@ -643,7 +639,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
         const unsigned long long c0 = prof ? clock64() : 0;
         if (kb >= S) mbar_wait(b_empty(s), ((kb / S) - 1) & 1, p.spin_limit, p.dbg, 0x110000u | kb);
         if (prof) qt_wait += clock64() - c0;
-        const uint32_t bytes = (PASSES >= 2 && !(PASSES == 3 && p.bsplit)) ? b_stage : b_plane;
+        const uint32_t bytes = b_stage;  // fp32 hi [+ lo, or bf16 hi + lo] planes, one contiguous block
         const float *src = p.wt + ((long long)(cb_base * p.taps + kb) * p.mtiles + mt) * (bytes / 4);
         if (leader) {
           if (p.mode & 8) {
@@ -690,8 +686,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
           const int kb = i * taps + t;
           const int s = kb % S;
           c0 = prof ? clock64() : 0;
-          mbar_wait((PASSES == 3 && p.bsplit) ? b_ready(s) : b_full(s), (kb / S) & 1, p.spin_limit, p.dbg,
-                    0x220000u | kb);
+          mbar_wait(b_full(s), (kb / S) & 1, p.spin_limit, p.dbg, 0x220000u | kb);
           if (prof) mt_wait += clock64() - c0;
           tc_fence_after();
           const uint64_t a0 = a_buf_desc + (uint64_t)((ky * wp + kx) & 0xFFFF);  // tap shift: 16 B per position
@@ -799,23 +794,6 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full(buf));
       if (prof) lt_fill += clock64() - c0;
-      if (PASSES == 3 && p.bsplit) {
-        // lo planes of this block's filter tiles, as they land
-        for (int t = 0; t < p.taps; t++) {
-          const int kb = i * p.taps + t;
-          const int s = kb % S;
-          if (lane == 0) mbar_wait(b_full(s), (kb / S) & 1, p.spin_limit, p.dbg, 0x320000u | kb);
-          __syncwarp();
-          const uint32_t sb = bring_base + (uint32_t)s * b_stage;
-          for (uint32_t o = lt * 16u; o < b_plane; o += LOADERS * 16u) {
-            const float4 a = lds128(sb + o);
-            sts128(sb + b_plane + o, make_float4(tf32_lo(a.x), tf32_lo(a.y), tf32_lo(a.z), tf32_lo(a.w)));
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(b_ready(s));
-        }
-      }
     }
     if (prof) { p.dbg[7] = (unsigned)lt_wait; p.dbg[8] = (unsigned)lt_fill; p.dbg[13] = (unsigned)(clock64() - lt_start); }
     // ------------------------------------------------------------------ epilogue
