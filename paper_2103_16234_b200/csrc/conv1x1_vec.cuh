@@ -26,9 +26,10 @@
 
 namespace b2c {
 
-// VEC = false: planes with H*W % 4 != 0 (7x7 GoogLeNet 5a/5b, 27x27): the
-// same register/shared mapping, pixels staged by 4-byte cp.async with a
-// per-pixel image offset (a 4-pixel group may straddle two images) and
+// VEC = false: planes with H*W % 4 != 0 (7x7 GoogLeNet 5a/5b, 27x27) and
+// stride-S 1x1 layers (ResNet projection shortcuts): the same register /
+// shared mapping, pixels staged by 4-byte cp.async with a per-pixel input
+// offset (subsampled by S; a 4-pixel group may straddle two images) and
 // scalar output stores.
 template <int WM, int WP, int BC>
 struct Vec1x1Tile {
@@ -61,8 +62,9 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP,
   const int m0 = mt * BM;
   const int q0 = pt * BP;
   const int split = blockIdx.y;
-  const int hw = p.HoWo;  // == H*W (1x1, stride 1, no padding)
-  const long long chw = (long long)p.C * hw;
+  const int hw = p.HoWo;            // output plane (== input plane for VEC: 1x1, stride 1, no padding)
+  const int in_hw = p.H * p.W;      // input plane (!VEC may subsample: stride S, no padding)
+  const long long chw = (long long)p.C * in_hw;
 
   // per-thread 16-byte pixel groups of a chunk: global offset relative to the
   // chunk's first channel (or -1 beyond the last pixel)
@@ -82,7 +84,10 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP,
       const int qe = q + e;
       if (gi < T::XG && qe < p.Q) {
         const int n = qe / hw;
-        xoff[k][e] = (Off)((long long)n * chw + (long long)c * hw + (qe - n * hw));
+        const int r = qe - n * hw;
+        const int oy = r / p.Wo;
+        const int ox = r - oy * p.Wo;
+        xoff[k][e] = (Off)((long long)n * chw + (long long)c * in_hw + (long long)oy * p.S * p.W + ox * p.S);
       } else {
         xoff[k][e] = -1;
       }
@@ -99,7 +104,7 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP,
   auto load_chunk = [&](int chunk, float *stage) {
     const int c0 = chunk * BC;
     const int cvalid = min(BC, p.C - c0);
-    const float *xsrc = p.x + (long long)c0 * hw;
+    const float *xsrc = p.x + (long long)c0 * in_hw;
 #pragma unroll
     for (int k = 0; k < T::XG_PER_THREAD; k++) {
       if (xdst[k] < 0) continue;

@@ -85,6 +85,7 @@ const Family kFamilies[] = {
     B2C_VEC1X1("fused_1x1v_m64p128", 2, 2, 16),
     B2C_VEC1X1("fused_1x1v_m128", 4, 2, 16),
     // pointwise, 4-byte pixel staging (1x1, stride 1, no padding, any H*W)
+    // (and strided 1x1, e.g. ResNet projection shortcuts)
     B2C_SCA1X1("fused_1x1s_m32", 1, 4, 16),
     B2C_SCA1X1("fused_1x1s_m64", 2, 4, 16),
     B2C_SCA1X1("fused_1x1s_m64p128", 2, 2, 16),
@@ -292,7 +293,7 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
   if (f.kind == 1)
     return g.HF == 1 && g.WF == 1 && g.S == 1 && g.PH == 0 && g.PW == 0 && ((long long)g.H * g.W) % 4 == 0;
   if (f.kind == 2)
-    return g.HF == 1 && g.WF == 1 && g.S == 1 && g.PH == 0 && g.PW == 0 && ((long long)g.H * g.W) % 4 != 0 &&
+    return g.HF == 1 && g.WF == 1 && g.PH == 0 && g.PW == 0 && (g.S != 1 || ((long long)g.H * g.W) % 4 != 0) &&
            (long long)g.N * g.C * g.H * g.W < (1LL << 31);
   if (stage1) return g.S == 1;
   if (f.hf == 0) return true;  // generic

@@ -177,6 +177,7 @@ def _torch_ops(cfg, seed=0):
 PLAN_CASES = [
     pk.ConvConfig("p3", n=3, c=37, h=14, w=14, m=40, hf=3, wf=3, pad_h=1, pad_w=1),
     pk.ConvConfig("p1", n=5, c=70, h=7, w=7, m=50, hf=1, wf=1),
+    pk.ConvConfig("p1s2", n=3, c=40, h=14, w=13, m=36, hf=1, wf=1, stride=2),
     pk.ConvConfig("p5", n=2, c=20, h=13, w=11, m=33, hf=5, wf=5, pad_h=2, pad_w=2),
     pk.ConvConfig("ps2", n=2, c=24, h=15, w=15, m=20, hf=3, wf=3, stride=2, pad_h=1, pad_w=1),
     pk.ConvConfig("p7", n=2, c=3, h=30, w=30, m=20, hf=7, wf=7, stride=2, pad_h=3, pad_w=3),
