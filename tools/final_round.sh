@@ -1,0 +1,15 @@
+#!/bin/bash
+# round-end evidence: smoke, GPU suite, bench (both arms), extra workloads, launch list
+OUT=gpurun_out/${1:-final}; mkdir -p $OUT
+export PYTHONUNBUFFERED=1
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+timeout 1200 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
+timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+for wl in c1 c3 c4 c5; do
+  timeout 900 python bench.py --workload $wl --steps 10 --warmup 3 --e2e-steps 1 --no-cpu-baseline > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+  python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
+echo done > $OUT/DONE
