@@ -33,7 +33,12 @@ def launches(path):
     for r in rd:
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        v = float(r["Metric Value"].replace(",", ""))
+        try:
+            v = float(r["Metric Value"].replace(",", ""))
+        except ValueError:
+            continue
+        if v != v:  # nan (ncu could not time the launch)
+            continue
         unit = r.get("Metric Unit", "ns")
         scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(unit, 1.0)
         name = re.sub(r"\(.*", "", r["Kernel Name"]).strip()
