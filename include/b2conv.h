@@ -133,7 +133,10 @@ typedef struct {
   int32_t m_halves;         /* out: 128-pixel UMMA M halves per tile (mode 2:
                                1 or 2, sharing each filter tile)              */
   int32_t bf16_corrections; /* out: 3xTF32 correction products run as bf16
-                               MMAs (K=16, twice the tf32 rate; mode 2)       */
+                               MMAs (K=16, twice the tf32 rate)               */
+  int32_t k_packed;         /* out: mode 1 with few input channels: the
+                               reduction runs over ceil(c*hf*wf/16) blocks of
+                               16 (channel, tap) pairs                        */
 } b2c_tc_plan;
 
 /* ---------------------------------------------------------------- metadata */

@@ -56,7 +56,7 @@ class TcPlanC(ctypes.Structure):
                 ("tmem_columns", ctypes.c_int32), ("flattened", ctypes.c_int32), ("passes", ctypes.c_int32),
                 ("grid", ctypes.c_int64), ("splits", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64),
                 ("mode", ctypes.c_int32), ("halo_positions", ctypes.c_int32), ("m_halves", ctypes.c_int32),
-                ("bf16_corrections", ctypes.c_int32)]
+                ("bf16_corrections", ctypes.c_int32), ("k_packed", ctypes.c_int32)]
 
 
 _P = ctypes.POINTER

@@ -470,6 +470,7 @@ b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_pl
   out->halo_positions = pl.halo;
   out->m_halves = pl.mh;
   out->bf16_corrections = pl.bf16corr ? 1 : 0;
+  out->k_packed = pl.kpack ? 1 : 0;
   return B2C_OK;
 }
 

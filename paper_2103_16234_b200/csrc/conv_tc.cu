@@ -58,7 +58,8 @@ bool tc_supported(const Geom &g) {
 }
 
 long long tc_filter_bytes(const Geom &g, const TcPlan &pl) {
-  const long long b = 4LL * cdiv(g.C, tc::BC) * tc::BC * g.HF * g.WF * (long long)pl.mtiles * pl.nf * pl.wplanes;
+  const long long k = pl.kpack ? cdiv((long long)g.C * g.HF * g.WF, tc::BC) * tc::BC : cdiv(g.C, tc::BC) * tc::BC * g.HF * g.WF;
+  const long long b = 4LL * k * (long long)pl.mtiles * pl.nf * pl.wplanes;
   return (b + 255) / 256 * 256;
 }
 
@@ -128,12 +129,16 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
   if (best_px < 0) return false;
   const int rc = 32 / xw;
   const long long nchunks = (long long)g.N * cdiv(ho, rc) * cdiv(wo, xw);
-  const int taps = g.HF * g.WF;
-  const int cblocks = (int)cdiv(g.C, tc::BC);
+  const int taps_geom = g.HF * g.WF;
+  // K packing (gather mode): few input channels waste most of each 16-channel
+  // k-block, so the reduction runs over (channel, tap) pairs instead
+  const bool kpack = g.C < tc::BC && taps_geom > 1 && forced_mode != 2;
+  const int taps = kpack ? 1 : taps_geom;
+  const int cblocks = (int)cdiv((long long)g.C * (kpack ? taps_geom : 1), tc::BC);
   const int KB = cblocks * taps;
   const int sms = device_sm_count(0);
   // halo mode (stride 1): tiles over the flattened padded stack
-  const bool halo_ok = g.S == 1 && forced_mode != 1;
+  const bool halo_ok = g.S == 1 && forced_mode != 1 && !kpack;
   const long long Wp = (long long)g.W + 2 * g.PW, Hp = (long long)g.H + 2 * g.PH;
 
   TcPlan best;
@@ -220,6 +225,7 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
           best.abufs = abufs;
           best.wplanes = planes;  // filter lo plane streamed with the hi plane
           best.bf16corr = bf16corr;
+          best.kpack = kpack;
           best.nf = nf;
           best.mtiles = mtiles;
           best.stages = stages;
@@ -247,8 +253,11 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
 
 cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const float *w, float *y, void *workspace,
                       long long ws_bytes, cudaStream_t stream) {
-  const int taps = g.HF * g.WF;
-  const int cblocks = (int)cdiv(g.C, tc::BC);
+  // K packing: filters [m][c][ky][kx] are already [m][k] with k = c*taps + tap,
+  // so they pre-tile as a 1x1 layer over C*taps virtual channels
+  const int taps = pl.kpack ? 1 : g.HF * g.WF;
+  const int cvirt = pl.kpack ? g.C * g.HF * g.WF : g.C;
+  const int cblocks = (int)cdiv(cvirt, tc::BC);
   const int Mp = pl.mtiles * pl.nf;
   if (!workspace || ws_bytes < tc_workspace_bytes(g, pl)) return cudaErrorInvalidValue;
   float *wt = static_cast<float *>(workspace);
@@ -259,12 +268,12 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
     const long long total = (long long)cblocks * taps * Mp * tc::BC;
     const int blocks = (int)std::min<long long>(cdiv(total, 256), 8LL * device_sm_count(0));
     note_launch();
-    tc::filter_tile_bf16corr_kernel<<<blocks, 256, 0, stream>>>(w, wt, g.M, g.C, taps, pl.nf, pl.mtiles, cblocks);
+    tc::filter_tile_bf16corr_kernel<<<blocks, 256, 0, stream>>>(w, wt, g.M, cvirt, taps, pl.nf, pl.mtiles, cblocks);
   } else {
     const long long total = (long long)cblocks * taps * Mp * tc::BC * planes;
     const int blocks = (int)std::min<long long>(cdiv(total, 256), 8LL * device_sm_count(0));
     note_launch();
-    tc::filter_tile_kernel<<<blocks, 256, 0, stream>>>(w, wt, g.M, g.C, taps, pl.nf, pl.mtiles, cblocks, planes);
+    tc::filter_tile_kernel<<<blocks, 256, 0, stream>>>(w, wt, g.M, cvirt, taps, pl.nf, pl.mtiles, cblocks, planes);
   }
   {
     cudaError_t e = cudaGetLastError();
@@ -304,9 +313,11 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   p.PW = g.PW;
   p.WF = g.WF;
   p.taps = taps;
+  p.kpack = pl.kpack ? 1 : 0;
+  p.taps_full = g.HF * g.WF;
   p.NF = pl.nf;
   p.mtiles = pl.mtiles;
-  p.cblocks = (int)cdiv(g.C, tc::BC);
+  p.cblocks = cblocks;
   p.stages = pl.stages;
   p.b_bytes = pl.nf * 64 * planes;
   p.stage_bytes = pl.stage_bytes;

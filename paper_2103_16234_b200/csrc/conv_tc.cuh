@@ -75,6 +75,7 @@ struct TcParams {
   long long nchunks; // N * rgroups * xblocks
   int PH, PW, WF, taps;
   int NF, mtiles, cblocks, Mp;
+  int kpack, taps_full;      // gather mode K packing: k-blocks of 16 (channel, tap) pairs; taps == 1 then
   int splits, kb_per_split;  // split-K over k-blocks (blockIdx.y); partial planes summed by stage2_sum_kernel
   float *partials;           // [split][n][m][ho][wo] when splits > 1
   long long part_stride;
@@ -431,6 +432,23 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
     const int Hh = p.flat ? 1 : p.H;  // flattened 1x1: one "row" of H*W pixels
     const int Ww = p.flat ? p.HW : p.W;
     auto gather = [&](int kb, float (&v)[CH_PER_LOADER]) {
+      if (p.kpack) {
+        // K packing (few input channels, e.g. a 7x7 stem on RGB): the reduction
+        // index k = c*taps + tap runs contiguously over (channel, tap) pairs, so
+        // a k-block holds 16 of them instead of 16 mostly-padding channels
+        const int k0 = (kb_base + kb) * BC + cgrp * CH_PER_LOADER;
+#pragma unroll
+        for (int j = 0; j < CH_PER_LOADER; j++) {
+          const int k = k0 + j;
+          const int c = k / p.taps_full;
+          const int t = k - c * p.taps_full;
+          const int ky = t / p.WF, kx = t - (t / p.WF) * p.WF;
+          const int iy = iy0 + ky, ix = ix0 + kx;
+          const bool ok = pbase >= 0 && c < p.C && iy >= 0 && iy < Hh && ix >= 0 && ix < Ww;
+          v[j] = ok ? __ldg(xg + pbase + (long long)c * p.HW + iy * Ww + ix) : 0.0f;
+        }
+        return;
+      }
       const int cb = (kb_base + kb) / p.taps;
       const int t = (kb_base + kb) - cb * p.taps;
       const int ky = t / p.WF;

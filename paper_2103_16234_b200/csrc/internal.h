@@ -34,7 +34,8 @@ struct TcPlan {
   int mh = 1;        // halo mode: 128-position M halves per tile
   int abufs = 0;     // halo mode: staged halo buffers (ring depth)
   int wplanes = 1;   // pre-tiled filter planes streamed from HBM/L2 (gather 3xTF32: hi + lo)
-  bool bf16corr = false;  // 3xTF32 halo mode: correction products as bf16 MMAs (K=16, twice the rate)
+  bool bf16corr = false;
+  bool kpack = false;     // gather mode: k-blocks over (channel, tap) pairs (few input channels)  // 3xTF32 halo mode: correction products as bf16 MMAs (K=16, twice the rate)
   int nf = 0;        // output channels per tile (UMMA N)
   int mtiles = 0;
   int stages = 0, stage_bytes = 0, smem_bytes = 0, tmem_cols = 0;

@@ -96,7 +96,8 @@ class ConvLayer:
             t = self._tc
             shape = f"h{t.halo_positions}" if t.mode == 2 else f"x{t.pixels_per_chunk}"
             return (f"{self.engine}_{shape}_n{t.filters_per_tile}_s{t.stages}_k{t.splits}"
-                    + ("_flat" if t.flattened else "") + ("_b16c" if t.bf16_corrections else ""))
+                    + ("_flat" if t.flattened else "") + ("_b16c" if t.bf16_corrections else "")
+                    + ("_kpack" if t.k_packed else ""))
         return self._lib.b2c_family_name(self._tiles.family).decode()
 
     @property

@@ -304,6 +304,9 @@ def test_tensor_core_planner_covers_every_baseline_layer(native):
                     flat = cfg.hf == cfg.wf == 1 and cfg.stride == 1 and cfg.pad_h == cfg.pad_w == 0
                     assert bool(p.flattened) == flat
                     kb = -(-cfg.c // 16) * cfg.hf * cfg.wf
+                    assert bool(p.k_packed) == (cfg.c < 16 and cfg.hf * cfg.wf > 1)
+                    if p.k_packed:
+                        kb = -(-(cfg.c * cfg.hf * cfg.wf) // 16)
                     assert p.mode in (1, 2)
                     if p.mode == 1:  # gather: 128-pixel tiles of 32-pixel chunks
                         width = ho * wo if flat else wo
