@@ -24,6 +24,10 @@ inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 const void *tc_kernel(int passes, bool halo, int mh) {
   if (!halo && passes == 2) return reinterpret_cast<const void *>(&tc::conv_tc_kernel<2>);
   if (halo) {
+    if (mh == 4)
+      return passes == 3 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<3, 4>)
+           : passes == 2 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<2, 4>)
+                         : reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<1, 4>);
     if (mh == 2)
       return passes == 3 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<3, 2>)
            : passes == 2 ? reinterpret_cast<const void *>(&tc::conv_tc_halo_kernel<2, 2>)
@@ -150,9 +154,9 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
   const int max_kbps = passes == 3 ? 72 : 1 << 30;
   const double out_bytes = 4.0 * g.N * g.M * g.HoWo;
   const int planes = passes == 3 ? 2 : 1;
-  // modes: 1 = gather; 2 = halo with one 128-position M half; 3 = halo with two
-  for (int mode = 1; mode <= 3; mode++) {
-    const int mh = mode == 3 ? 2 : 1;
+  // modes: 1 = gather; 2 / 3 / 4 = halo with 1 / 2 / 4 128-position M slices
+  for (int mode = 1; mode <= 4; mode++) {
+    const int mh = mode == 4 ? 4 : mode == 3 ? 2 : 1;
     if (forced_mode > 0 && (mode == 1) != (forced_mode == 1)) continue;
     if (mode >= 2 && !halo_ok) continue;
     const long long halo = (tc::TILE_P * mh + (g.HF - 1) * Wp + (g.WF - 1) + 7) / 8 * 8;
@@ -193,7 +197,7 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
         const int splits = (int)cdiv(units, ups);
         if (splits != sp && forced_splits <= 0) continue;  // duplicate of a smaller split
         const int kbps = mode == 1 ? ups : ups * taps;
-        if (kbps > max_kbps && forced_splits <= 0 && !(mode == 2 && ups == 1)) continue;
+        if (kbps > max_kbps && forced_splits <= 0 && !(mode >= 2 && ups == 1)) continue;
         const long long ctas = ptiles * mtiles * splits;
         // per-k-block clocks (B200 measurements): tensor issue ~95 clk per
         // 128x256x8 tf32 UMMA; gather mode adds a ~1.1-1.3k clk latency chain
@@ -210,7 +214,7 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
           // per tap: tensor issue, the L2 feed of the filter tile (~36 B/clk/SM
           // of the ~6.3 KB/clk chip L2 rate), ~150 clk of barrier work
           const double l2 = nf * 64.0 * planes / 36.0;  // hi (+ streamed lo) plane
-          const double fill = 400.0 + halo * 4.0 / 512.0 * 60.0;
+          const double fill = 500.0 + halo * 10.0;  // measured ~2.4 clk per (position, 4-channel) item
           t_cta = ups * std::max(taps * (std::max(mma, l2) + 150.0), fill);
         }
         t_cta += 6000.0 + nf * 8.0;

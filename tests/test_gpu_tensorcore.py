@@ -160,7 +160,7 @@ def test_tensor_core_split_k_within_tolerance_and_deterministic(engine):
         assert oracle.relative_error(a, ref) <= tol(cfg, engine), (sp, layer.family)
 
 
-@pytest.mark.parametrize("wl,name", [("c4", "vgg4_2"), ("c5", "layer3.1.conv2"), ("c3", "alexnet-conv2"),
+@pytest.mark.parametrize("wl,name", [("c4", "vgg4_2"), ("c5", "layer3.1.conv2"), ("c3", "alexnet-conv2"), ("c5", "layer1.0.conv2"),
                                      ("c2", "4e-1x1"), ("c5", "conv1")])
 def test_tensor_core_full_size_layers_sampled_images(wl, name):
     """BASELINE full sizes, checked on a seeded sample of images (images are
