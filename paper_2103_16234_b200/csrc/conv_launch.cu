@@ -69,11 +69,14 @@ const Family kFamilies[] = {
     B2C_FAMILY("fused_1x1s2_m64", 1, 1, 2, 64, 256, 16, false),
     B2C_FAMILY("fused_1x1s2_m128", 1, 1, 2, 128, 256, 16, false),
     B2C_FAMILY("fused_3x3s1_m32", 3, 3, 1, 32, 256, 8, false),
+    B2C_FAMILY("fused_3x3s1_m32p128", 3, 3, 1, 32, 128, 8, false),  // small tiles: latency-bound batch-1 layers
+    B2C_FAMILY("fused_3x3s1_m64p128", 3, 3, 1, 64, 128, 8, false),
     B2C_FAMILY("fused_3x3s1_m64", 3, 3, 1, 64, 256, 8, false),
     B2C_FAMILY("fused_3x3s1_m128", 3, 3, 1, 128, 256, 8, false),
     B2C_FAMILY("fused_3x3s2_m64", 3, 3, 2, 64, 256, 8, false),
     B2C_FAMILY("fused_3x3s2_m128", 3, 3, 2, 128, 256, 8, false),
     B2C_FAMILY("fused_5x5s1_m32", 5, 5, 1, 32, 256, 4, false),
+    B2C_FAMILY("fused_5x5s1_m32p128", 5, 5, 1, 32, 128, 4, false),
     B2C_FAMILY("fused_5x5s1_m64", 5, 5, 1, 64, 256, 4, false),
     B2C_FAMILY("fused_5x5s1_m128", 5, 5, 1, 128, 256, 4, false),
     B2C_FAMILY("fused_7x7s2_m64", 7, 7, 2, 64, 256, 4, false),
@@ -81,6 +84,7 @@ const Family kFamilies[] = {
     B2C_FAMILY("fused_generic_m32", 0, 0, 0, 32, 256, 4, false),
     // pointwise 16-byte families (1x1, stride 1, no padding, H*W % 4 == 0)
     B2C_VEC1X1("fused_1x1v_m32", 1, 4, 16),
+    B2C_VEC1X1("fused_1x1v_m32p128", 1, 2, 16),
     B2C_VEC1X1("fused_1x1v_m64", 2, 4, 16),
     B2C_VEC1X1("fused_1x1v_m64p128", 2, 2, 16),
     B2C_VEC1X1("fused_1x1v_m128", 4, 2, 16),

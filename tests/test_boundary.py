@@ -381,3 +381,27 @@ def test_harness_csv_header_is_reference_prefix_and_skips(tmp_path):
     assert lines[0].startswith(H.CSV_HEADER + ",") and lines[1].startswith("s2,twostage,1,0,,,,,skipped(Unsupported: stride)")
     with pytest.raises(pk.ConvKitError):
         H.emit_report([], out)
+
+
+def test_harness_analyze_plan_dump_runs_on_host(tmp_path):
+    """``analyze`` (reference cli.py:97-120): reference ANALYZE_HEADER prefix,
+    the reference plan in its columns, the B200 plan of every engine after it;
+    planner-only, so it runs without a GPU."""
+    from paper_2103_16234_b200 import harness as H
+
+    assert H.ANALYZE_HEADER == ("config,batch,blocks,threads_per_block,split,dot_products_per_thread,"
+                                "warps_total,transactions_total,txn_per_warp,perfectly_coalesced_warps")
+    out = tmp_path / "plans.csv"
+    assert H.main(["analyze", "--batches", "1,8", "--algos", "fused,twostage,tf32x3", "--out", str(out)]) == 0
+    lines = out.read_text().splitlines()
+    assert lines[0] == H.ANALYZE_HEADER + "," + H.ANALYZE_GPU_COLUMNS
+    rows = [l.split(",") for l in lines[1:]]
+    presets = pk.preset_configs()
+    assert len(rows) == len(presets) * 2 * 3  # every preset is stride 1: all three engines plan
+    for r, cfg in zip(rows[::6], presets):
+        plan = pk.plan_launch(cfg.with_batch(1))
+        assert r[0] == cfg.name and r[2:6] == [str(plan.blocks), str(plan.threads_per_block),
+                                               str(plan.split_per_filter_row), str(plan.dot_products_per_thread)]
+    for r in rows:
+        assert r[10] in ("fused", "twostage", "tf32x3") and r[11] and int(r[12]) > 0 and int(r[14]) >= 1
+    assert H.main(["analyze", "--algos", "winograd", "--out", str(out)]) == 1

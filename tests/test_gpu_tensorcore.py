@@ -229,3 +229,16 @@ def test_harness_run_bench_validates_every_engine(tmp_path):
     H.emit_report(recs, tmp_path / "r.csv")
     H.emit_report(recs, tmp_path / "r.md", "md")
     assert (tmp_path / "r.csv").read_text().count("\n") == len(recs) + 1
+
+
+def test_harness_cli_validate_and_run(tmp_path, capsys):
+    """``validate`` / ``run`` subcommands (reference cli.py:123-145): exit 0, one ok line per run."""
+    from paper_2103_16234_b200 import harness as H
+
+    assert H.main(["validate", "--algos", "fused,twostage,tf32x3", "--batches", "1"]) == 0
+    out = capsys.readouterr().out
+    assert out.count("ok   ") == len(pk.preset_configs()) * 3 and "FAIL" not in out
+    rep = tmp_path / "r.csv"
+    assert H.main(["run", "--algos", "fused,tf32", "--batches", "2", "--repeats", "2", "--baseline", "fused",
+                   "--out", str(rep)]) == 0
+    assert rep.read_text().count("\n") == len(pk.preset_configs()) * 2 + 1
