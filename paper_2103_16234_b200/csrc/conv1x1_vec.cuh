@@ -44,6 +44,29 @@ struct Vec1x1Tile {
   static constexpr int MIN_BLOCKS = NT >= 512 ? 1 : 512 / NT;
 };
 
+// split-C through DSMEM (see cluster_reduce_tile in conv_kernel.cuh): park the
+// accumulator tile [BM][BP] in this CTA's shared memory, then reduce.
+template <int BM, int BP, int NT>
+__device__ __forceinline__ void vec_cluster_epilogue(const KParams &p, const float2 (&acc)[4][8], float *tile,
+                                                     int m0, int q0, int wrow, int xcol) {
+  __syncthreads();  // every warp is done with the pipeline stages the tile overwrites
+#pragma unroll
+  for (int g = 0; g < 2; g++)
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const int pr = r >> 1;
+      const bool hi = r & 1;
+      float4 v;
+      v.x = hi ? acc[pr][4 * g + 0].y : acc[pr][4 * g + 0].x;
+      v.y = hi ? acc[pr][4 * g + 1].y : acc[pr][4 * g + 1].x;
+      v.z = hi ? acc[pr][4 * g + 2].y : acc[pr][4 * g + 2].x;
+      v.w = hi ? acc[pr][4 * g + 3].y : acc[pr][4 * g + 3].x;
+      const int row = wrow + (r & 3) + (r >> 2) * 16;
+      *reinterpret_cast<float4 *>(tile + row * BP + xcol + 32 * g) = v;
+    }
+  cluster_reduce_tile<BM, BP, NT>(p, tile, m0, q0);
+}
+
 template <int WM, int WP, int BC, bool VEC = true>
 __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP, BC>::MIN_BLOCKS)
     conv1x1_vec_kernel(const KParams p) {
@@ -189,6 +212,14 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP,
   }
   if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
+  if (p.cluster) {
+    vec_cluster_epilogue<BM, BP, NT>(p, acc, smem, m0, q0, wrow, xcol);
+    if (p.trace && tid == 0) {
+      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      p.trace[5 * cta + 4] = global_ns();
+    }
+    return;
+  }
   // epilogue: 4 consecutive pixels per (channel, group) -> one 16-byte store
   // (VEC), or four scalar stores that may straddle two images
   float *dst = p.splits > 1 ? p.partials + (long long)split * p.part_stride : p.y;

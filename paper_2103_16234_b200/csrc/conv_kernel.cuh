@@ -70,6 +70,7 @@ struct KParams {
   unsigned long long *trace;  // optional per-CTA (smid, t_start, t_tables, t_loop, t_end) records
   unsigned long long mRS, mHp, mHoWo, mWo;  // exact division magics: floor(2^32/d) + 1
   int pdl;                    // launched with programmatic dependent launch
+  int cluster;                // split-C partials reduced through DSMEM: the splits of a tile form one cluster
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -99,6 +100,75 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// --- split-C reduction inside a thread-block cluster ---------------------------
+// The `splits` CTAs of one output tile (blockIdx.y = channel range) launch as
+// one cluster (dims 1 x splits x 1).  Each CTA has parked its accumulator tile
+// [BM][BP] (row = output channel, column = output pixel) at the base of its
+// shared memory; after a cluster barrier, rank r sums slice r of the tile over
+// ranks 0..splits-1 in ascending order (every add rounded, +0.0 start: the
+// sum stage2_sum_kernel forms from partial planes, so results are bitwise
+// identical) and stores it.  No partial planes in HBM, no second kernel.
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(unsigned local_addr, unsigned rank) {
+  unsigned remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(remote)
+               : "memory");
+  return v;
+}
+
+template <int BM, int BP, int NT>
+__device__ __forceinline__ void cluster_reduce_tile(const KParams &p, const float *tile, int m0, int q0) {
+  cluster_barrier();
+  constexpr int F4 = BM * BP / 4;
+  const int S = p.splits;
+  const int per = (F4 + S - 1) / S;
+  const int lo = (int)cluster_rank() * per;
+  const int hi = min(F4, lo + per);
+  const unsigned tile_sa = (unsigned)__cvta_generic_to_shared(tile);
+  const int hw = p.HoWo;
+  // 16-byte stores when 4 consecutive pixels always share an image and y is aligned
+  const bool vec = (hw & 3) == 0 && (reinterpret_cast<uintptr_t>(p.y) & 15) == 0;
+  for (int i = lo + (int)threadIdx.x; i < hi; i += NT) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < S; s++) {
+      const float4 v = ld_dsmem_f4(tile_sa + 16u * (unsigned)i, (unsigned)s);
+      a.x = __fadd_rn(a.x, v.x);
+      a.y = __fadd_rn(a.y, v.y);
+      a.z = __fadd_rn(a.z, v.z);
+      a.w = __fadd_rn(a.w, v.w);
+    }
+    const int row = i / (BP / 4);
+    const int q = q0 + (i - row * (BP / 4)) * 4;
+    const int m = m0 + row;
+    if (m >= p.M || q >= p.Q) continue;
+    if (vec) {
+      const int n = q / hw;
+      *reinterpret_cast<float4 *>(p.y + (long long)n * p.M * hw + (long long)m * hw + (q - n * hw)) = a;
+    } else {
+      const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int qe = q + e;
+        if (qe >= p.Q) break;
+        const int n = qe / hw;
+        p.y[(long long)n * p.M * hw + (long long)m * hw + (qe - n * hw)] = av[e];
+      }
+    }
+  }
+  cluster_barrier();  // keep this CTA's tile alive until every rank has read it
 }
 
 // HF_T/WF_T/S_T == 0 -> taken from the runtime parameters (generic family).
@@ -380,6 +450,17 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
   }
   const long long plane = p.HoWo;
 
+  if (p.cluster) {  // split-C through DSMEM (cluster_reduce_tile)
+    cp_async_wait<0>();
+    __syncthreads();  // the tile overwrites the halo tables and pipeline stages
+#pragma unroll
+    for (int i = 0; i < RM; i++)
+#pragma unroll
+      for (int j = 0; j < RP; j++) smem[(mg * RM + i) * BP + j * NTP + tp] = acc_at(i, j);
+    cluster_reduce_tile<BM, BP, NT>(p, smem, m0, q0);
+    trace_end();
+    return;
+  }
   // splits == 1: fully overwrite y.  splits > 1: this channel range's partial
   // goes to plane `split` of the workspace (y layout); stage2_sum_kernel then
   // adds the planes in ascending order (deterministic, no atomics).

@@ -103,6 +103,7 @@ constexpr int kNumFamilies = sizeof(kFamilies) / sizeof(kFamilies[0]);
 int g_sm_count = -1;
 std::mutex g_mu;
 bool g_attr_done[kNumFamilies][64] = {};
+std::unordered_map<long long, int> g_cluster_ok;  // (family, splits, device) -> cluster launch feasible
 
 int sm_count_of(int device) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -283,6 +284,11 @@ bool pdl_enabled() {
   return on;
 }
 
+bool cluster_reduce_enabled() {
+  static const bool on = std::getenv("B2C_NO_CLUSTER") == nullptr;
+  return on;
+}
+
 const char *family_name(int id) {
   if (id < 0 || id >= kNumFamilies) return "invalid";
   return kFamilies[id].name;
@@ -396,6 +402,10 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
       e = cudaFuncSetAttribute(f.kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                (int)cudaSharedmemCarveoutMaxShared);
       if (e != cudaSuccess) return e;
+      if (!f.strict) {  // split-C clusters of up to 16 CTAs (non-portable above 8)
+        e = cudaFuncSetAttribute(f.kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+      }
       g_attr_done[tc.family][dev] = true;
     }
   }
@@ -442,27 +452,74 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   const long long nctas = tc.grid * tc.splits * tc.grid_z;
   unsigned long long *trace = nullptr;
   if (trace_file && cudaMalloc(&trace, sizeof(unsigned long long) * 5 * nctas) == cudaSuccess) p.trace = trace;
+  // split-C through DSMEM: the splits of one output tile launch as a cluster
+  // (at most 16 CTAs; the cluster must fit the GPU)
+  int smem = tc.smem_bytes;
+  if (!stage1 && !f.strict && tc.splits > 1 && tc.splits <= 16 && cluster_reduce_enabled()) {
+    const int tile_bytes = tc.bm * tc.bp * (int)sizeof(float);
+    const int csmem = std::max(smem, tile_bytes);
+    const long long key = ((long long)tc.family * 64 + tc.splits) * 64 + dev;
+    int ok = -1;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      auto it = g_cluster_ok.find(key);
+      if (it != g_cluster_ok.end()) ok = it->second;
+    }
+    if (ok < 0) {
+      cudaLaunchConfig_t qc = {};
+      qc.gridDim = grid;
+      qc.blockDim = dim3(tc.threads);
+      qc.dynamicSmemBytes = (size_t)csmem;
+      cudaLaunchAttribute ca[1];
+      ca[0].id = cudaLaunchAttributeClusterDimension;
+      ca[0].val.clusterDim.x = 1;
+      ca[0].val.clusterDim.y = (unsigned)tc.splits;
+      ca[0].val.clusterDim.z = 1;
+      qc.attrs = ca;
+      qc.numAttrs = 1;
+      int nclusters = 0;
+      ok = (cudaOccupancyMaxActiveClusters(&nclusters, f.kernel, &qc) == cudaSuccess && nclusters > 0) ? 1 : 0;
+      cudaGetLastError();  // a refused query is not a launch error
+      std::lock_guard<std::mutex> lk(g_mu);
+      g_cluster_ok[key] = ok;
+    }
+    if (ok) {
+      p.cluster = 1;
+      smem = csmem;
+    }
+  }
   void *args[] = {&p};
   note_launch();
   cudaError_t err;
-  if (p.pdl) {
+  if (p.pdl || p.cluster) {
     // programmatic dependent launch: this grid's prologue may overlap the tail of
     // the previous kernel on the stream (the kernel waits before reading inputs)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(tc.threads);
-    cfg.dynamicSmemBytes = (size_t)tc.smem_bytes;
+    cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (p.pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      na++;
+    }
+    if (p.cluster) {
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = 1;
+      attr[na].val.clusterDim.y = (unsigned)tc.splits;
+      attr[na].val.clusterDim.z = 1;
+      na++;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     err = cudaLaunchKernelExC(&cfg, f.kernel, args);
   } else {
-    err = cudaLaunchKernel(f.kernel, grid, dim3(tc.threads), args, (size_t)tc.smem_bytes, stream);
+    err = cudaLaunchKernel(f.kernel, grid, dim3(tc.threads), args, (size_t)smem, stream);
   }
-  if (err == cudaSuccess && tc.splits > 1 && !stage1)
+  if (err == cudaSuccess && tc.splits > 1 && !stage1 && !p.cluster)
     err = launch_stage2(p.partials, y, p.part_stride, tc.splits, dev, stream);
   if (trace) {
     std::vector<unsigned long long> h(5 * nctas);

@@ -14,6 +14,7 @@
 from __future__ import annotations
 
 import hashlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -21,6 +22,8 @@ import pytest
 from conftest import cfg_from
 
 import paper_2103_16234_b200 as pk
+
+ROOT = Path(__file__).resolve().parents[1]
 
 pytestmark = pytest.mark.gpu
 
@@ -297,3 +300,58 @@ def test_full_size_layers_sampled_images(wl, name):
         ref = oracle.conv_f64(one, x[img:img + 1].cpu().numpy(), wn)
         assert oracle.relative_error(y[img:img + 1].cpu().numpy(), ref) <= tol(cfg), img
     torch.cuda.synchronize()
+
+
+_CLUSTER_SCRIPT = r"""
+import sys, numpy as np, torch
+import paper_2103_16234_b200 as pk
+sys.path.insert(0, "tests")
+from test_gpu_parity import CLUSTER_CASES, _torch_ops
+outs = {}
+for cfg in CLUSTER_CASES:
+    x, w = _torch_ops(cfg, seed=7)
+    for fam in pk.matching_families(cfg):
+        for splits in (2, 3, 5, 8, 12, 16):
+            try:
+                layer = pk.ConvLayer(cfg, family=fam, splits=splits)
+            except pk.InvalidPlan:
+                continue
+            outs[f"{cfg.name}|{layer.family}|{layer.splits}"] = layer(x, w).cpu().numpy()
+np.savez(sys.argv[1], **outs)
+"""
+
+CLUSTER_CASES = PLAN_CASES[:5] + [
+    pk.ConvConfig("c1x1big", n=2, c=512, h=14, w=14, m=130, hf=1, wf=1),
+    pk.ConvConfig("c3big", n=1, c=256, h=28, w=28, m=70, hf=3, wf=3, pad_h=1, pad_w=1),
+    pk.ConvConfig("c1x1odd", n=3, c=300, h=7, w=7, m=64, hf=1, wf=1),
+]
+
+
+def test_cluster_split_reduction_bitwise_equals_partial_planes(tmp_path):
+    """Split-C through DSMEM clusters (default) against the partial-planes +
+    stage2_sum path (B2C_NO_CLUSTER=1): the same ascending-order sum, so the
+    outputs must be bitwise identical for every family and split count."""
+    import os
+    import subprocess
+    import sys
+
+    res = {}
+    for tag, env in (("cluster", {}), ("planes", {"B2C_NO_CLUSTER": "1"})):
+        out = tmp_path / f"{tag}.npz"
+        r = subprocess.run([sys.executable, "-c", _CLUSTER_SCRIPT, str(out)], cwd=ROOT, capture_output=True,
+                           text=True, env={**os.environ, **env}, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res[tag] = dict(np.load(out))
+    assert res["cluster"].keys() == res["planes"].keys() and len(res["cluster"]) > 20
+    bad = [k for k in res["cluster"] if res["cluster"][k].tobytes() != res["planes"][k].tobytes()]
+    assert not bad, bad
+    # and the cluster path is one kernel (no stage-2 launch)
+    from paper_2103_16234_b200 import _native as nat
+
+    cfg = CLUSTER_CASES[-3]
+    x, w = _torch_ops(cfg)
+    layer = pk.ConvLayer(cfg, family=pk.matching_families(cfg)[0], splits=8)
+    assert layer.splits == 8
+    nat.lib().b2c_reset_launch_count()
+    layer(x, w)
+    assert nat.lib().b2c_launch_count() == 1
