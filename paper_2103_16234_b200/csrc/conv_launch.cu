@@ -284,8 +284,12 @@ bool pdl_enabled() {
   return on;
 }
 
+// Split-C through DSMEM clusters is opt-in (B2C_CLUSTER=1): measured on B200 it
+// loses to partial planes + stage 2 (C2 26.1 vs 29.9 TFLOP/s; 4e-1x1 65.9 vs
+// 45.8 us) because cross-CTA DSMEM reads run at ~20 B/clk per SM, so parking a
+// 32-64 KB tile costs more than the L2-resident partial planes.
 bool cluster_reduce_enabled() {
-  static const bool on = std::getenv("B2C_NO_CLUSTER") == nullptr;
+  static const bool on = std::getenv("B2C_CLUSTER") != nullptr;
   return on;
 }
 
