@@ -427,7 +427,10 @@ def tensor_core_variant(args, lib, nat, cfgs, xs, ws, ys, world, device, local_r
     workload and operands, reported separately with its stated tolerance.
     Roofline: tensor-bound against the tf32 dense rate, taken as half the
     measured cuBLAS bf16 burst rate (MEASURED_PEAKS.json; B200 dense
-    tf32:bf16 = 1:2), divided by 3 for 3xTF32 (three tf32 MMAs per product)."""
+    tf32:bf16 = 1:2), divided by the MMA work per product: 3 for 3xTF32 with
+    tf32 corrections, 2 when the two correction products run as bf16 MMAs
+    (each at twice the tf32 rate: 1 + 1/2 + 1/2), 1 for plain tf32 —
+    flop-weighted over the layers' plans."""
     from paper_2103_16234_b200 import ConvLayer
 
     eng = args.tc_engine
@@ -442,6 +445,8 @@ def tensor_core_variant(args, lib, nat, cfgs, xs, ws, ys, world, device, local_r
     pk = peaks()
     tf32_peak = pk.get("bf16_tflops", 1590.0) / 2.0
     passes = 3 if eng == "tf32x3" else 1
+    units = [(1.0 if eng == "tf32" else (2.0 if L._tc.bf16_corrections else 3.0)) for L in layers]
+    unit_eq = sum(c.flops * u for c, u in zip(cfgs, units)) / flops  # tf32 MMA passes per product
     achieved = flops / (kern_ms * 1e-3) / 1e12
     e2e = None
     if args.e2e_steps > 0:
@@ -450,10 +455,11 @@ def tensor_core_variant(args, lib, nat, cfgs, xs, ws, ys, world, device, local_r
             "unit": "GFLOP/s", "ms_per_step": round(ms_total / args.steps, 4), "tolerance": TC_TOLERANCE[eng],
             "dtype": "tf32x3 (fp32 operands split hi+lo, fp32 accumulate in TMEM)" if passes == 3 else "tf32",
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3),
-                         "peak": round(tf32_peak / passes, 3), "unit": "TFLOP/s",
-                         "frac": round(achieved * passes / tf32_peak, 4), "traffic": None,
+                         "peak": round(tf32_peak / unit_eq, 3), "unit": "TFLOP/s",
+                         "frac": round(achieved * unit_eq / tf32_peak, 4), "traffic": None,
                          "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (dense tf32 rate)"
-                                         + (" / 3 (3xTF32)" if passes == 3 else "")),
+                                         + (f" / {unit_eq:.2f} (3xTF32: tf32 hi*hi + bf16 or tf32 correction "
+                                            "MMAs, flop-weighted over the plans)" if passes == 3 else "")),
                          "kernel_ms_per_step": round(kern_ms, 4)},
             "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches * args.steps,
             "per_layer": [{"layer": c.name, "us": round(t * 1e3, 2), "gflops": round(c.flops / (t * 1e-3) / 1e9, 1),
