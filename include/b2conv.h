@@ -91,6 +91,11 @@ typedef struct {
                            on input to b2c_select_tiles / b2c_conv2d_forward,
                            > 0 forces the split                              */
   int64_t workspace_bytes; /* workspace the plan needs (0 unless splits > 1) */
+  int32_t reduce;       /* split-C reduction (splits > 1): 1 = partial planes in
+                           the workspace + a stage-2 sum kernel, 2 = inside a
+                           thread-block cluster through DSMEM (one kernel; same
+                           ascending-order sum, bitwise identical).  On input
+                           0 = planner's choice, 1 / 2 force a mode.          */
 } b2c_tile_plan;
 
 typedef enum {
@@ -173,10 +178,11 @@ b2c_status b2c_block_position_ranges(int64_t work, int64_t split, int64_t *lo_hi
 b2c_status b2c_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tile_plan *out);
 
 /* Register a measured plan (tools/autotune.py "find" result) for an exact
- * shape: the planner then uses (family, splits) for it instead of its cost
+ * shape: the planner then uses (family, splits, reduce) for it instead of its cost
  * model.  The Python package registers paper_2103_16234_b200/tuned_plans.json
  * at import. */
-b2c_status b2c_register_tuned_plan(const b2c_conv_desc *d, int32_t engine, int32_t family, int32_t splits);
+b2c_status b2c_register_tuned_plan(const b2c_conv_desc *d, int32_t engine, int32_t family, int32_t splits,
+                                   int32_t reduce);
 
 /* ------------------------------------------------- device-pointer compute */
 /* Fused direct convolution (any stride >= 1, any padding).  Replaces the

@@ -47,7 +47,7 @@ class TilePlanC(ctypes.Structure):
                 ("bc", ctypes.c_int32), ("threads", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("smem_rows", ctypes.c_int32), ("smem_row_stride", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_int32), ("grid", ctypes.c_int64), ("splits", ctypes.c_int32),
-                ("workspace_bytes", ctypes.c_int64)]
+                ("workspace_bytes", ctypes.c_int64), ("reduce", ctypes.c_int32)]
 
 
 class TcPlanC(ctypes.Structure):
@@ -78,7 +78,8 @@ SIGNATURES = {
     "b2c_validate_plan": (ctypes.c_int, [_P(ConvDesc), _P(DeviceModelC), _P(LaunchPlanC)]),
     "b2c_block_position_ranges": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, _P(ctypes.c_int64)]),
     "b2c_select_tiles": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, _P(TilePlanC)]),
-    "b2c_register_tuned_plan": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    "b2c_register_tuned_plan": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                               ctypes.c_int32]),
     "b2c_conv2d_forward": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, ctypes.c_void_p, ctypes.c_int64,
                                           _P(TilePlanC), ctypes.c_void_p]),
     "b2c_conv2d_forward_tc": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, ctypes.c_void_p, ctypes.c_int64,
@@ -155,7 +156,8 @@ def _register_tuned(l) -> None:
             continue
         d = ConvDesc(*[int(v) for v in e["desc"]])
         eng = ENGINE_TWOSTAGE if e.get("engine") == "twostage" else ENGINE_FUSED
-        l.b2c_register_tuned_plan(ctypes.byref(d), eng, names.index(e["family"]), int(e.get("splits", 1)))
+        l.b2c_register_tuned_plan(ctypes.byref(d), eng, names.index(e["family"]), int(e.get("splits", 1)),
+                                  int(e.get("reduce", 0)))
 
 
 def last_error() -> str:

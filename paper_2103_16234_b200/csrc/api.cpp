@@ -113,9 +113,11 @@ struct PlanKey {
   int forced_splits;
   int allow_split;
   int allow_vec;
+  int forced_reduce;
   bool operator==(const PlanKey &o) const {
     return std::memcmp(&d, &o.d, sizeof(d)) == 0 && stage1 == o.stage1 && device == o.device && forced == o.forced &&
-           forced_splits == o.forced_splits && allow_split == o.allow_split && allow_vec == o.allow_vec;
+           forced_splits == o.forced_splits && allow_split == o.allow_split && allow_vec == o.allow_vec &&
+           forced_reduce == o.forced_reduce;
   }
 };
 struct PlanKeyHash {
@@ -130,7 +132,7 @@ std::mutex g_plan_mu;
 std::unordered_map<PlanKey, b2c::TileChoice, PlanKeyHash> g_plans;
 
 b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, int forced, int forced_splits,
-                     bool allow_split, b2c::TileChoice *tc, bool allow_vec = true) {
+                     bool allow_split, b2c::TileChoice *tc, bool allow_vec = true, int forced_reduce = 0) {
   int device = 0;
   cudaGetDevice(&device);
   PlanKey key;
@@ -142,6 +144,7 @@ b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, in
   key.forced_splits = forced_splits;
   key.allow_split = allow_split;
   key.allow_vec = allow_vec;
+  key.forced_reduce = forced_reduce;
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_plans.find(key);
@@ -150,10 +153,10 @@ b2c_status get_tiles(const b2c_conv_desc *d, const b2c::Geom &g, bool stage1, in
       return B2C_OK;
     }
   }
-  if (!b2c::plan_tiles(g, stage1, device, forced, forced_splits, allow_split, allow_vec, tc)) {
-    if (forced >= 0 || forced_splits > 0)
-      return fail(B2C_INVALID_PLAN, "tile family %d (%s) / split %d cannot run this configuration", forced,
-                  forced >= 0 ? b2c::family_name(forced) : "auto", forced_splits);
+  if (!b2c::plan_tiles(g, stage1, device, forced, forced_splits, allow_split, allow_vec, tc, forced_reduce)) {
+    if (forced >= 0 || forced_splits > 0 || forced_reduce > 0)
+      return fail(B2C_INVALID_PLAN, "tile family %d (%s) / split %d / reduce %d cannot run this configuration",
+                  forced, forced >= 0 ? b2c::family_name(forced) : "auto", forced_splits, forced_reduce);
     return fail(B2C_UNSUPPORTED, "no kernel family fits this configuration (shared-memory halo too large)");
   }
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -174,6 +177,7 @@ void export_tiles(const b2c::TileChoice &tc, b2c_tile_plan *out) {
   out->grid = tc.grid * tc.splits * tc.grid_z;
   out->splits = tc.splits;
   out->workspace_bytes = tc.ws_bytes;
+  out->reduce = tc.reduce;
 }
 
 b2c_status resolve_plan(const b2c_conv_desc *d, const b2c_launch_plan *plan, const b2c_device_model *dev,
@@ -372,22 +376,25 @@ b2c_status b2c_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tile_pla
   if ((st = check_sizes(g)) != B2C_OK) return st;
   if (engine == B2C_ENGINE_TWOSTAGE && d->stride != 1)
     return fail(B2C_UNSUPPORTED, "two-stage convolution requires stride 1, got %d", d->stride);
+  if (out->reduce < 0 || out->reduce > 2) return fail(B2C_INVALID_ARGUMENT, "reduce must be 0, 1 or 2, got %d", out->reduce);
   b2c::TileChoice tc;
   st = get_tiles(d, g, engine == B2C_ENGINE_TWOSTAGE, out->family >= 0 ? out->family : -1,
-                 out->splits > 0 ? out->splits : 0, true, &tc);
+                 out->splits > 0 ? out->splits : 0, true, &tc, true, out->reduce);
   if (st != B2C_OK) return st;
   export_tiles(tc, out);
   return B2C_OK;
 }
 
-b2c_status b2c_register_tuned_plan(const b2c_conv_desc *d, int32_t engine, int32_t family, int32_t splits) {
+b2c_status b2c_register_tuned_plan(const b2c_conv_desc *d, int32_t engine, int32_t family, int32_t splits,
+                                   int32_t reduce) {
   b2c_status st = check_config(d, nullptr);
   if (st != B2C_OK) return st;
   b2c::Geom g = geom_of(d);
   const bool stage1 = engine == B2C_ENGINE_TWOSTAGE;
   if (!b2c::family_matches(family, g, stage1))
     return fail(B2C_INVALID_PLAN, "family %d cannot run this configuration", family);
-  b2c::register_tuned(g, stage1, family, splits);
+  if (reduce < 0 || reduce > 2) return fail(B2C_INVALID_ARGUMENT, "reduce must be 0, 1 or 2, got %d", reduce);
+  b2c::register_tuned(g, stage1, family, splits, reduce);
   std::lock_guard<std::mutex> lk(g_plan_mu);
   g_plans.clear();  // cached plans may predate the registration
   return B2C_OK;
@@ -407,8 +414,9 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
   if ((st = check_sizes(g)) != B2C_OK) return st;
   const int forced = (tiles && tiles->family >= 0) ? tiles->family : -1;
   const int forced_splits = (tiles && tiles->splits > 0) ? tiles->splits : 0;
+  const int forced_reduce = (tiles && tiles->reduce > 0 && tiles->reduce <= 2) ? tiles->reduce : 0;
   b2c::TileChoice tc;
-  st = get_tiles(d, g, false, forced, forced_splits, true, &tc);
+  st = get_tiles(d, g, false, forced, forced_splits, true, &tc, true, forced_reduce);
   if (st != B2C_OK) return st;
   const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
                          reinterpret_cast<uintptr_t>(workspace)) & 15) == 0;
@@ -419,7 +427,7 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
   if (tc.kind == 1 && !aligned && forced >= 0)
     return fail(B2C_INVALID_ARGUMENT, "family %s needs 16-byte aligned x, y and workspace", b2c::family_name(forced));
   if (!ws_ok || (tc.kind == 1 && !aligned)) {
-    st = get_tiles(d, g, false, forced, ws_ok ? forced_splits : 0, ws_ok, &tc, aligned);
+    st = get_tiles(d, g, false, forced, ws_ok ? forced_splits : 0, ws_ok, &tc, aligned, forced_reduce);
     if (st != B2C_OK) return st;
   }
   cudaError_t e = b2c::launch_direct(g, tc, x, w, y, false, 0, workspace, (cudaStream_t)stream);

@@ -329,34 +329,43 @@ struct TunedHash {
     return h;
   }
 };
-std::unordered_map<TunedKey, std::pair<int, int>, TunedHash> g_tuned;
+struct TunedPlan {
+  int family = -1, splits = 0, reduce = 0;
+};
+std::unordered_map<TunedKey, TunedPlan, TunedHash> g_tuned;
 std::mutex g_tuned_mu;
 
 TunedKey tuned_key(const Geom &g, bool stage1) {
   return TunedKey{{g.N, g.C, g.H, g.W, g.M, g.HF, g.WF, g.S, g.PH, g.PW, stage1 ? 1 : 0}};
 }
 
-void register_tuned(const Geom &g, bool stage1, int family, int splits) {
+void register_tuned(const Geom &g, bool stage1, int family, int splits, int reduce) {
   std::lock_guard<std::mutex> lk(g_tuned_mu);
-  g_tuned[tuned_key(g, stage1)] = {family, splits};
+  TunedPlan t;
+  t.family = family;
+  t.splits = splits;
+  t.reduce = reduce;
+  g_tuned[tuned_key(g, stage1)] = t;
 }
 
 // Planner: returns false if no family can run the geometry.
-bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int forced_splits, bool allow_split,
-                bool allow_vec, TileChoice *out) {
+namespace {
+bool plan_tiles_core(const Geom &g, bool stage1, int device, int forced_family, int forced_splits, bool allow_split,
+                     bool allow_vec, TileChoice *out, int *tuned_reduce) {
   const int sms = sm_count_of(device);
   Candidate best;
   if (forced_family < 0 && forced_splits <= 0) {
-    std::pair<int, int> t{-1, 0};
+    TunedPlan t;
     {
       std::lock_guard<std::mutex> lk(g_tuned_mu);
       auto it = g_tuned.find(tuned_key(g, stage1));
       if (it != g_tuned.end()) t = it->second;
     }
-    if (t.first >= 0 && (allow_split || t.second <= 1) && (allow_vec || kFamilies[t.first].kind == 0) &&
-        family_matches(t.first, g, stage1) &&
-        evaluate(g, t.first, stage1, sms, t.second, allow_split, &best)) {
+    if (t.family >= 0 && (allow_split || t.splits <= 1) && (allow_vec || kFamilies[t.family].kind == 0) &&
+        family_matches(t.family, g, stage1) &&
+        evaluate(g, t.family, stage1, sms, t.splits, allow_split, &best)) {
       *out = best.tc;
+      *tuned_reduce = t.reduce;
       return true;
     }
   }
@@ -382,6 +391,36 @@ bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int f
   }
   if (best.family < 0) return false;
   *out = best.tc;
+  return true;
+}
+}  // namespace
+
+// Split-C reduction mode: forced by the caller, else the tuned plan's, else
+// partial planes + stage 2 (B2C_CLUSTER=1 makes DSMEM clusters the default).
+// Clusters hold at most 16 CTAs and need the tile [BM][BP] in shared memory.
+bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int forced_splits, bool allow_split,
+                bool allow_vec, TileChoice *out, int forced_reduce) {
+  int tuned_reduce = 0;
+  if (!plan_tiles_core(g, stage1, device, forced_family, forced_splits, allow_split, allow_vec, out, &tuned_reduce))
+    return false;
+  int r = 0;
+  if (out->splits > 1 && !stage1) {
+    r = forced_reduce > 0 ? forced_reduce : (tuned_reduce > 0 ? tuned_reduce : (cluster_reduce_enabled() ? 2 : 1));
+    if (r == 2 && out->splits > 16) {
+      if (forced_reduce == 2) return false;
+      r = 1;
+    }
+  }
+  out->reduce = r;
+  if (r == 2) {
+    const long long tile_bytes = 4LL * out->bm * out->bp;
+    if (tile_bytes > 226 * 1024) {
+      if (forced_reduce == 2) return false;
+      out->reduce = 1;
+    } else {
+      out->smem_bytes = (int)std::max<long long>(out->smem_bytes, tile_bytes);
+    }
+  }
   return true;
 }
 
@@ -459,10 +498,10 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   // split-C through DSMEM: the splits of one output tile launch as a cluster
   // (at most 16 CTAs; the cluster must fit the GPU)
   int smem = tc.smem_bytes;
-  if (!stage1 && !f.strict && tc.splits > 1 && tc.splits <= 16 && cluster_reduce_enabled()) {
+  if (!stage1 && !f.strict && tc.splits > 1 && tc.splits <= 16 && tc.reduce == 2) {
     const int tile_bytes = tc.bm * tc.bp * (int)sizeof(float);
     const int csmem = std::max(smem, tile_bytes);
-    const long long key = ((long long)tc.family * 64 + tc.splits) * 64 + dev;
+    const long long key = ((((long long)tc.family * 32 + tc.splits) * 64 + dev) << 18) + csmem;
     int ok = -1;
     {
       std::lock_guard<std::mutex> lk(g_mu);

@@ -24,6 +24,7 @@ struct TileChoice {
   int splits = 1;       // fused: channel ranges reduced separately
   int chunks_per_split = 0;
   long long ws_bytes = 0;  // workspace needed for splits > 1 (partial planes)
+  int reduce = 0;          // splits > 1: 1 = partial planes + stage-2 kernel, 2 = DSMEM cluster reduction
   double cost = 0;
 };
 
@@ -63,13 +64,13 @@ int num_families();
 bool family_matches(int fam_id, const Geom &g, bool stage1);
 int device_sm_count(int device);
 bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int forced_splits, bool allow_split,
-                bool allow_vec, TileChoice *out);
+                bool allow_vec, TileChoice *out, int forced_reduce = 0);
 cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, const float *w, float *y,
                           bool stage1, long long y_tap_stride, void *workspace, cudaStream_t stream);
 cudaError_t launch_stage2(const float *partials, float *y, long long total, int taps, int device,
                           cudaStream_t stream);
 bool pdl_enabled();
-void register_tuned(const Geom &g, bool stage1, int family, int splits);
+void register_tuned(const Geom &g, bool stage1, int family, int splits, int reduce = 0);
 void note_launch();
 
 }  // namespace b2c

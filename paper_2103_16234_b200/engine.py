@@ -57,7 +57,7 @@ class ConvLayer:
     """A resolved forward convolution for one configuration."""
 
     def __init__(self, cfg: ConvConfig, engine: str = "fused", family: int = -1, splits: int = 0,
-                 filters_per_tile: int = 0, tc_mode: int = 0):
+                 filters_per_tile: int = 0, tc_mode: int = 0, reduce: int = 0):
         if engine not in nat.ENGINES:
             raise ValueError(f"unknown engine {engine!r}")
         if engine == "twostage" and cfg.stride != 1:
@@ -69,6 +69,7 @@ class ConvLayer:
         self._tiles = nat.TilePlanC()
         self._tiles.family = int(family)
         self._tiles.splits = int(splits)
+        self._tiles.reduce = int(reduce)  # split-C: 0 planner, 1 partial planes + stage 2, 2 DSMEM cluster
         self._engine_id = nat.ENGINES[engine]
         self.tensor_core = engine in ("tf32x3", "tf32")
         if self.tensor_core:
@@ -98,11 +99,17 @@ class ConvLayer:
             return (f"{self.engine}_{shape}_n{t.filters_per_tile}_s{t.stages}_k{t.splits}"
                     + ("_flat" if t.flattened else "") + ("_b16c" if t.bf16_corrections else "")
                     + ("_kpack" if t.k_packed else ""))
-        return self._lib.b2c_family_name(self._tiles.family).decode()
+        name = self._lib.b2c_family_name(self._tiles.family).decode()
+        return name + ("_dsm" if self._tiles.splits > 1 and self._tiles.reduce == 2 else "")
 
     @property
     def grid(self) -> int:
         return int(self._tc.grid if self.tensor_core else self._tiles.grid)
+
+    @property
+    def reduce(self) -> int:
+        """Split-C reduction of the plan: 0 none, 1 partial planes + stage 2, 2 DSMEM cluster."""
+        return 0 if self.tensor_core else int(self._tiles.reduce)
 
     @property
     def splits(self) -> int:

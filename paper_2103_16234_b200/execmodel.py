@@ -80,6 +80,7 @@ class TilePlan:
     grid: int
     splits: int
     workspace_bytes: int
+    reduce: int = 0  # split-C reduction: 0 none, 1 partial planes + stage 2, 2 DSMEM cluster
 
 
 def _plan_from_c(p: nat.LaunchPlanC) -> LaunchPlan:
@@ -137,13 +138,15 @@ def matching_families(cfg: ConvConfig, engine: str = "fused") -> list[int]:
     return [i for i in range(l.b2c_num_families()) if l.b2c_family_matches(ctypes.byref(d), e, i)]
 
 
-def select_tiles(cfg: ConvConfig, engine: str = "fused", family: int = -1, splits: int = 0) -> TilePlan:
-    """The B200 tile plan for ``cfg`` (planner's choice, or a forced family / split)."""
+def select_tiles(cfg: ConvConfig, engine: str = "fused", family: int = -1, splits: int = 0,
+                 reduce: int = 0) -> TilePlan:
+    """The B200 tile plan for ``cfg`` (planner's choice, or a forced family / split / reduction)."""
     out = nat.TilePlanC()
     out.family = int(family)
     out.splits = int(splits)
+    out.reduce = int(reduce)
     e = nat.ENGINE_TWOSTAGE if engine == "twostage" else nat.ENGINE_FUSED
     nat.check(nat.lib().b2c_select_tiles(ctypes.byref(nat.desc(cfg)), e, ctypes.byref(out)))
     return TilePlan(nat.lib().b2c_family_name(out.family).decode(), int(out.family), int(out.bm), int(out.bp),
                     int(out.bc), int(out.threads), int(out.stages), int(out.smem_rows), int(out.smem_row_stride),
-                    int(out.smem_bytes), int(out.grid), int(out.splits), int(out.workspace_bytes))
+                    int(out.smem_bytes), int(out.grid), int(out.splits), int(out.workspace_bytes), int(out.reduce))

@@ -405,3 +405,34 @@ def test_harness_analyze_plan_dump_runs_on_host(tmp_path):
     for r in rows:
         assert r[10] in ("fused", "twostage", "tf32x3") and r[11] and int(r[12]) > 0 and int(r[14]) >= 1
     assert H.main(["analyze", "--algos", "winograd", "--out", str(out)]) == 1
+
+
+def test_split_reduction_mode_plumbing():
+    """b2c_tile_plan.reduce: planner default = partial planes + stage 2 (1);
+    forced DSMEM cluster (2) for <= 16 splits and tiles that fit shared
+    memory, InvalidPlan beyond; tuned plans carry their mode."""
+    import ctypes
+
+    from paper_2103_16234_b200 import _native as nat
+
+    cfg = pk.ConvConfig("red", n=2, c=512, h=14, w=14, m=130, hf=1, wf=1)
+    assert pk.select_tiles(cfg, splits=1).reduce == 0
+    p1, p2 = pk.select_tiles(cfg, splits=8, reduce=1), pk.select_tiles(cfg, splits=8, reduce=2)
+    assert (p1.reduce, p2.reduce) == (1, 2) and p2.smem_bytes >= 4 * p2.bm * p2.bp
+    assert pk.select_tiles(cfg, splits=8).reduce in (1, 2)
+    assert pk.select_tiles(cfg, splits=32).reduce == 1
+    with pytest.raises(pk.InvalidPlan):
+        pk.select_tiles(cfg, splits=32, reduce=2)
+    with pytest.raises(pk.ConvKitError):
+        pk.select_tiles(cfg, splits=8, reduce=3)
+    one = pk.ConvConfig("red1", n=3, c=520, h=14, w=14, m=130, hf=1, wf=1)
+    fam = pk.select_tiles(one, splits=4).family_id
+    lib = nat.lib()
+    assert lib.b2c_register_tuned_plan(ctypes.byref(nat.desc(one)), nat.ENGINE_FUSED, fam, 4, 2) == nat.OK
+    auto = pk.select_tiles(one)
+    assert (auto.family_id, auto.splits, auto.reduce) == (fam, 4, 2)
+    assert pk.ConvLayer(one).family.endswith("_dsm")
+    assert lib.b2c_register_tuned_plan(ctypes.byref(nat.desc(one)), nat.ENGINE_FUSED, fam, 4, 7) != nat.OK
+    twostage = pk.select_tiles(pk.ConvConfig("t", n=1, c=64, h=8, w=8, m=8, hf=3, wf=3, pad_h=1, pad_w=1),
+                               engine="twostage")
+    assert twostage.reduce == 0

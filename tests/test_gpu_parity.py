@@ -302,33 +302,6 @@ def test_full_size_layers_sampled_images(wl, name):
     torch.cuda.synchronize()
 
 
-_CLUSTER_SCRIPT = r"""
-import sys, numpy as np, torch
-import paper_2103_16234_b200 as pk
-sys.path.insert(0, "tests")
-from test_gpu_parity import CLUSTER_CASES, _torch_ops
-outs = {}
-for cfg in CLUSTER_CASES:
-    x, w = _torch_ops(cfg, seed=7)
-    for fam in pk.matching_families(cfg):
-        for splits in (2, 3, 5, 8, 12, 16):
-            try:
-                layer = pk.ConvLayer(cfg, family=fam, splits=splits)
-            except pk.InvalidPlan:
-                continue
-            outs[f"{cfg.name}|{layer.family}|{layer.splits}"] = layer(x, w).cpu().numpy()
-from paper_2103_16234_b200 import _native as nat
-cfg = CLUSTER_CASES[-3]
-x, w = _torch_ops(cfg)
-layer = pk.ConvLayer(cfg, family=pk.matching_families(cfg)[0], splits=8)
-assert layer.splits == 8
-layer(x, w)
-nat.lib().b2c_reset_launch_count()
-layer(x, w)
-launches = np.array([nat.lib().b2c_launch_count()])
-np.savez(sys.argv[1], launches=launches, **outs)
-"""
-
 CLUSTER_CASES = PLAN_CASES[:5] + [
     pk.ConvConfig("c1x1big", n=2, c=512, h=14, w=14, m=130, hf=1, wf=1),
     pk.ConvConfig("c3big", n=1, c=256, h=28, w=28, m=70, hf=3, wf=3, pad_h=1, pad_w=1),
@@ -336,23 +309,32 @@ CLUSTER_CASES = PLAN_CASES[:5] + [
 ]
 
 
-def test_cluster_split_reduction_bitwise_equals_partial_planes(tmp_path):
-    """Split-C through DSMEM clusters (opt-in, B2C_CLUSTER=1) against the
-    default partial-planes + stage2_sum path: the same ascending-order sum, so
-    the outputs must be bitwise identical for every family and split count."""
-    import os
-    import subprocess
-    import sys
+@pytest.mark.parametrize("cfg", CLUSTER_CASES, ids=lambda c: c.name)
+def test_cluster_split_reduction_bitwise_equals_partial_planes(cfg):
+    """Split-C through DSMEM clusters (reduce=2) against partial planes +
+    stage2_sum (reduce=1): the same ascending-order sum, so the outputs are
+    bitwise identical for every family and split count; the cluster path is
+    one kernel, the planes path two."""
+    import torch
+    from paper_2103_16234_b200 import _native as nat
 
-    res = {}
-    for tag, env in (("cluster", {"B2C_CLUSTER": "1"}), ("planes", {})):
-        out = tmp_path / f"{tag}.npz"
-        r = subprocess.run([sys.executable, "-c", _CLUSTER_SCRIPT, str(out)], cwd=ROOT, capture_output=True,
-                           text=True, env={**os.environ, **env}, timeout=600)
-        assert r.returncode == 0, r.stderr[-3000:]
-        res[tag] = dict(np.load(out))
-    assert res["cluster"].keys() == res["planes"].keys() and len(res["cluster"]) > 20
-    bad = [k for k in res["cluster"] if k != "launches" and res["cluster"][k].tobytes() != res["planes"][k].tobytes()]
-    assert not bad, bad
-    # the cluster path is one kernel; partial planes add the stage-2 launch
-    assert int(res["cluster"]["launches"][0]) == 1 and int(res["planes"]["launches"][0]) == 2
+    x, w = _torch_ops(cfg, seed=7)
+    n = 0
+    for fam in pk.matching_families(cfg):
+        for splits in (2, 3, 5, 8, 12, 16):
+            try:
+                planes = pk.ConvLayer(cfg, family=fam, splits=splits, reduce=1)
+                dsm = pk.ConvLayer(cfg, family=fam, splits=splits, reduce=2)
+            except pk.InvalidPlan:
+                continue
+            if planes.splits != splits:
+                continue
+            assert dsm.reduce == 2 and dsm.family.endswith("_dsm") and planes.reduce == 1
+            a = planes(x, w)
+            nat.lib().b2c_reset_launch_count()
+            b = dsm(x, w)
+            assert nat.lib().b2c_launch_count() == 1
+            torch.cuda.synchronize()
+            assert a.cpu().numpy().tobytes() == b.cpu().numpy().tobytes(), (dsm.family, splits)
+            n += 1
+    assert n > 0

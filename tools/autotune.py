@@ -109,20 +109,22 @@ def main():
                 auto = ConvLayer(cfg)
                 y = torch.empty(auto.output_shape(), device="cuda")
                 t_auto = time_layer(auto, x, w, y)
-                best = (t_auto, auto.family, auto.splits)
+                best = (t_auto, names[auto._tiles.family], auto.splits, auto.reduce)
                 for f in matching_families(cfg):
                     for sp in (1, 2, 3, 4, 6, 8, 12, 16, 24):
-                        try:
-                            L = ConvLayer(cfg, family=f, splits=sp)
-                        except Exception:
-                            continue
-                        if L.splits != sp:
-                            continue
-                        t = time_layer(L, x, w, y)
-                        if t < best[0]:
-                            best = (t, names[f], L.splits)
+                        for red in ((0,) if sp == 1 else (1, 2) if sp <= 16 else (1,)):
+                            try:
+                                L = ConvLayer(cfg, family=f, splits=sp, reduce=red)
+                            except Exception:
+                                continue
+                            if L.splits != sp:
+                                continue
+                            t = time_layer(L, x, w, y)
+                            if t < best[0]:
+                                best = (t, names[f], L.splits, L.reduce)
                 rec = {"layer": f"{wl}/{cfg.name}/N{n}", "desc": list(key), "engine": "fused",
-                       "family": best[1], "splits": best[2], "us": round(best[0], 2), "model_us": round(t_auto, 2)}
+                       "family": best[1], "splits": best[2], "reduce": best[3], "us": round(best[0], 2),
+                       "model_us": round(t_auto, 2)}
                 print(json.dumps(rec), flush=True)
                 if best[0] < t_auto * 0.97:
                     plans.append(rec)

@@ -51,10 +51,10 @@ def main():
     plans = []
     for cfg in cfgs:
         L = ConvLayer(cfg)
-        plans.append((L._tiles.family, L.splits))
+        plans.append((L._tiles.family, L.splits, L.reduce))
 
     def measure(pl, reps=2):
-        layers = [ConvLayer(c, family=f, splits=s) for c, (f, s) in zip(cfgs, pl)]
+        layers = [ConvLayer(c, family=f, splits=s, reduce=r) for c, (f, s, r) in zip(cfgs, pl)]
         best = float("inf")
         for _ in range(reps):
             ms, _, _ = bench.time_graph(lib, layers, xs, ws, ys, targs, 1, dev, 0, groups)
@@ -69,26 +69,27 @@ def main():
         for i, cfg in enumerate(cfgs):
             if time.time() - t0 > a.budget_s:
                 break
-            f0, s0 = plans[i]
+            f0, s0, r0 = plans[i]
             cands = {(f0, s) for s in SPLITS}
             for f in matching_families(cfg):
                 for s in {s0, max(1, s0 // 2), s0 * 2}:
                     cands.add((f, s))
+            cands = {(f, s, r) for f, s in cands for r in ((0,) if s == 1 else (1, 2) if s <= 16 else (1,))}
             best = (cur, plans[i])
-            for f, s in sorted(cands):
-                if (f, s) == plans[i]:
+            for f, s, r in sorted(cands):
+                if (f, s, r) == plans[i]:
                     continue
                 try:
-                    L = ConvLayer(cfg, family=f, splits=s)
+                    L = ConvLayer(cfg, family=f, splits=s, reduce=r)
                 except Exception:  # noqa: BLE001
                     continue
                 if L.splits != s:
                     continue
                 trial = list(plans)
-                trial[i] = (f, s)
+                trial[i] = (f, s, L.reduce)
                 t = measure(trial)
                 if t < best[0] * 0.996:
-                    best = (t, (f, s))
+                    best = (t, (f, s, L.reduce))
             if best[1] != plans[i]:
                 trial = list(plans)
                 trial[i] = best[1]
@@ -98,8 +99,8 @@ def main():
                     plans = trial
                     cur = t_new
                     changed += 1
-                    print(json.dumps({"sweep": sweep, "layer": cfg.name, "from": [names[f0], s0],
-                                      "to": [names[best[1][0]], best[1][1]], "step_ms": round(t_new, 4),
+                    print(json.dumps({"sweep": sweep, "layer": cfg.name, "from": [names[f0], s0, r0],
+                                      "to": [names[best[1][0]], best[1][1], best[1][2]], "step_ms": round(t_new, 4),
                                       "was_ms": round(t_old, 4)}), flush=True)
                 else:
                     cur = t_old
@@ -108,9 +109,9 @@ def main():
             break
     final = measure(plans, 3)
     out = []
-    for cfg, (f, s) in zip(cfgs, plans):
+    for cfg, (f, s, r) in zip(cfgs, plans):
         out.append({"layer": f"{a.workload}/{cfg.name}/N{a.batch}", "desc": list(cfg.as_tuple()), "engine": "fused",
-                    "family": names[f], "splits": s, "us": None, "model_us": None, "step_ms": round(final, 4),
+                    "family": names[f], "splits": s, "reduce": r, "us": None, "model_us": None, "step_ms": round(final, 4),
                     "source": "tools/step_tune.py (dataflow step)"})
     with open(a.out, "w") as fh:
         json.dump({"generator": "tools/step_tune.py", "device": torch.cuda.get_device_name(), "start_ms": base0,
