@@ -237,6 +237,43 @@ def time_layers(layers, xs, ws, ys, reps=20):
     return out
 
 
+TRAFFIC_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+
+
+def dominant_kernel(cfgs, layers, layer_ms, workload):
+    """The kernel family with the largest share of the step's kernel time
+    (per-layer CUDA-event times on the launching stream, split-C sums
+    included): its algorithmic flop and bytes per launch, achieved TFLOP/s =
+    its layers' algorithmic flops / their summed time, and — when a committed
+    ncu capture of the same layers exists (profiles/r1_traffic.json, written
+    by tools/traffic.py) — the measured DRAM bytes per launch."""
+    fam = {}
+    for c, L, t in zip(cfgs, layers, layer_ms):
+        k = L.family.replace("_dsm", "")
+        e = fam.setdefault(k, {"ms": 0.0, "flops": 0, "bytes": 0, "layers": []})
+        e["ms"] += t
+        e["flops"] += c.flops
+        e["bytes"] += c.compulsory_bytes
+        e["layers"].append(c.name)
+    name, e = max(fam.items(), key=lambda kv: kv[1]["ms"])
+    n = len(e["layers"])
+    traffic, src = None, None
+    try:
+        with open(TRAFFIC_PATH) as fh:
+            rec = json.load(fh).get(workload, {})
+        got = [rec[l]["dram_bytes"] for l in e["layers"] if l in rec and rec[l].get("family", "").replace(
+            "_dsm", "") == name]
+        if len(got) == n:
+            traffic = round(sum(got) / n)
+            src = ("ncu dram__bytes_read.sum + dram__bytes_write.sum of the same layers and plans "
+                   "(cold cache, conv kernel + its split-C sum), mean per launch: " + os.path.basename(TRAFFIC_PATH))
+    except (OSError, ValueError, KeyError):
+        pass
+    return {"kernel": name, "achieved_tflops": e["flops"] / (e["ms"] * 1e-3) / 1e12,
+            "share": round(e["ms"] / sum(layer_ms), 4), "launches": n, "flop_per_launch": round(e["flops"] / n),
+            "bytes_per_launch": round(e["bytes"] / n), "traffic": traffic, "traffic_source": src}
+
+
 def time_cudnn(cfgs, xs, ws, reps=10):
     """cuDNN fp32 (TF32 disabled) through torch, per layer, best algorithm
     (benchmark mode) -- an external library baseline for the report only (the
@@ -523,6 +560,7 @@ def main():
     bytes_step = sum(c.compulsory_bytes for c in cfgs)
     per_layer = [{"layer": c.name, "us": round(t * 1e3, 2), "gflops": round(c.flops / (t * 1e-3) / 1e9, 1),
                   "family": L.family} for c, L, t in zip(cfgs, layers, layer_ms)]
+    dom = dominant_kernel(cfgs, layers, layer_ms, args.workload)
 
     # e2e: host buffers through the C-ABI drop-in (H2D x,w + kernel + D2H y per layer)
     e2e = None
@@ -555,14 +593,22 @@ def main():
                 "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic (uniform [-1,1) inputs and filters, torch RNG on device)",
                 "config": config,
-                "roofline": {"bound": "fp32", "achieved": round(achieved_tflops, 3), "peak": round(peak_tflops, 3),
-                             "unit": "TFLOP/s", "frac": round(achieved_tflops / peak_tflops, 4), "traffic": None,
+                "roofline": {"bound": "fp32", "achieved": round(dom["achieved_tflops"], 3),
+                             "peak": round(peak_tflops, 3), "unit": "TFLOP/s",
+                             "frac": round(dom["achieved_tflops"] / peak_tflops, 4), "traffic": dom["traffic"],
+                             "kernel": dom["kernel"], "kernel_share_of_step": dom["share"],
+                             "launches_per_step": dom["launches"],
+                             "algorithmic_flop_per_launch": dom["flop_per_launch"],
+                             "algorithmic_bytes_per_launch": dom["bytes_per_launch"],
+                             "traffic_source": dom["traffic_source"],
                              "peak_source": "b2c_probe_fp32_peak: FFMA2 register-blocked loop on all SMs, "
                                             f"measured live ({fpc.value:.1f} FMA/clk/SM at {mhz.value:.0f} MHz)",
-                             "frac_of_nominal_74.45": round(achieved_tflops / NOMINAL_FP32_TFLOPS, 4),
-                             "bytes_per_step": bytes_step,
-                             "hbm_frac": round(bytes_step / (kern_ms * 1e-3) / (hbm * 1e9), 4),
-                             "kernel_ms_per_step": round(kern_ms, 4)},
+                             "step": {"achieved": round(achieved_tflops, 3),
+                                      "frac": round(achieved_tflops / peak_tflops, 4),
+                                      "frac_of_nominal_74.45": round(achieved_tflops / NOMINAL_FP32_TFLOPS, 4),
+                                      "bytes_per_step": bytes_step,
+                                      "hbm_frac": round(bytes_step / (kern_ms * 1e-3) / (hbm * 1e9), 4),
+                                      "kernel_ms_per_step": round(kern_ms, 4)}},
                 "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
                 "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
                 "per_layer": per_layer, "tensor_core_variant": tc}

@@ -436,3 +436,31 @@ def test_split_reduction_mode_plumbing():
     twostage = pk.select_tiles(pk.ConvConfig("t", n=1, c=64, h=8, w=8, m=8, hf=3, wf=3, pad_h=1, pad_w=1),
                                engine="twostage")
     assert twostage.reduce == 0
+
+
+def test_bench_dominant_kernel_roofline_fields(tmp_path, monkeypatch):
+    """bench.py's roofline object is about the dominant kernel family: the one
+    with the largest share of the step's kernel time; traffic comes from the
+    committed ncu capture only when it covers exactly those layers."""
+    import json
+    import sys
+
+    sys.path.insert(0, str(pk.__file__).rsplit("/", 2)[0])
+    import bench
+    from paper_2103_16234_b200 import workloads as W
+
+    cfgs = W.layers("c2", 32)[:6]
+    layers = [pk.ConvLayer(c) for c in cfgs]
+    ms = [0.01] * len(cfgs)
+    ms[2] = 1.0  # one slow layer makes its family dominant
+    fam = layers[2].family.replace("_dsm", "")
+    idx = [i for i, L in enumerate(layers) if L.family.replace("_dsm", "") == fam]
+    path = tmp_path / "traffic.json"
+    path.write_text(json.dumps({"c2": {cfgs[i].name: {"family": layers[i].family, "dram_bytes": 1000 + i}
+                                       for i in idx}}))
+    monkeypatch.setattr(bench, "TRAFFIC_PATH", str(path))
+    d = bench.dominant_kernel(cfgs, layers, ms, "c2")
+    assert d["kernel"] == fam and d["launches"] == len(idx)
+    assert abs(d["achieved_tflops"] - sum(cfgs[i].flops for i in idx) / (sum(ms[i] for i in idx) * 1e-3) / 1e12) < 1e-9
+    assert d["traffic"] == round(sum(1000 + i for i in idx) / len(idx)) and d["traffic_source"]
+    assert bench.dominant_kernel(cfgs, layers, ms, "c3")["traffic"] is None  # no capture for that workload
