@@ -5,6 +5,12 @@ export PYTHONUNBUFFERED=1
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 timeout 1200 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+# measured DRAM traffic of every layer's launches (feeds the roofline "traffic" of the bench lines)
+timeout 1200 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+  -k regex:"conv_|stage2" --csv --log-file $OUT/traffic_ncu.csv python tools/traffic.py run c1,c2,c3,c4,c5 \
+  > $OUT/traffic_layers.json 2> $OUT/traffic.err
+python tools/traffic.py merge $OUT/traffic_layers.json $OUT/traffic_ncu.csv > $OUT/r1_traffic.json 2>> $OUT/traffic.err \
+  && cp $OUT/r1_traffic.json profiles/r1_traffic.json
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 for wl in c1 c3 c4 c5; do

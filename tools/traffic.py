@@ -50,7 +50,7 @@ def run(workloads):
 
 
 def merge(layers_path, ncu_csv):
-    order = json.load(open(layers_path))
+    order = json.loads([l for l in open(layers_path) if l.startswith("[")][-1])
     with open(ncu_csv) as fh:
         lines = [l for l in fh if not l.startswith("==")]
     per = {}
