@@ -18,4 +18,9 @@ for wl in c1 c3 c4 c5; do
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
+# one --set full capture of the top C2 layer's kernel and of the C1 kernel (plans as shipped)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"conv_" -c 1 --launch-skip 2 \
+  -o $OUT/c2_4e1x1 python tools/prof_layer.py c2 32 4e-1x1 > $OUT/ncu_c2.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"conv_" -c 1 --launch-skip 2 \
+  -o $OUT/c1 python tools/prof_layer.py c1 1 res-conv2x-3x3 > $OUT/ncu_c1.log 2>&1
 echo done > $OUT/DONE
