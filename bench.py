@@ -407,7 +407,41 @@ def time_graph(lib, layers, xs, ws, ys, args, world, device, local_rank, groups=
     return ms_local, launches_per_step, clk
 
 
+def gpu_local_cpus(index: int):
+    """CPUs on the GPU's NUMA node (NVML affinity mask), within this process's
+    allowed set; None if unknown."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = ((os.cpu_count() or 64) + 63) // 64
+        masks = pynvml.nvmlDeviceGetCpuAffinity(h, words)
+        cpus = {64 * i + b for i, m in enumerate(masks) for b in range(64) if (int(m) >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:  # noqa: BLE001 - binding is an optimisation, never a requirement
+        return None
+
+
 def e2e_run(lib, nat, cfgs, xs, ws, ys, engine_id, steps, world, device, local_rank):
+    """See _e2e_run; the host side (pinned buffers and the calling thread) is
+    bound to the GPU's NUMA node while it runs (first-touch placement of the
+    pinned pages next to the GPU's PCIe root), then the affinity is restored."""
+    saved = os.sched_getaffinity(0)
+    cpus = None if os.environ.get("B2C_NO_NUMA_BIND") else gpu_local_cpus(local_rank)
+    if cpus and cpus != saved:
+        os.sched_setaffinity(0, cpus)
+    try:
+        out = _e2e_run(lib, nat, cfgs, xs, ws, ys, engine_id, steps, world, device, local_rank)
+    finally:
+        os.sched_setaffinity(0, saved)
+    out["host_binding"] = (f"{len(cpus)} of {len(saved)} CPUs (GPU-local NUMA node)" if cpus and cpus != saved
+                           else "none")
+    return out
+
+
+def _e2e_run(lib, nat, cfgs, xs, ws, ys, engine_id, steps, world, device, local_rank):
     """Same metric through the host-buffer C-ABI: every step copies each
     layer's input and filters from pinned host memory, convolves, and copies
     the output back, all layers of the step in one b2c_conv_host_layers call

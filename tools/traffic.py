@@ -1,7 +1,7 @@
 """Measured DRAM traffic per layer for bench.py's roofline (GPU box, under ncu).
 
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-        --clock-control none -k regex:"conv_|stage2" --csv --log-file gpurun_out/tr/ncu.csv \
+        --clock-control none -k regex:"conv|stage2" --csv --log-file gpurun_out/tr/ncu.csv \
         python tools/traffic.py run c1,c2,c3,c4,c5 > gpurun_out/tr/layers.json
     python tools/traffic.py merge gpurun_out/tr/layers.json gpurun_out/tr/ncu.csv > profiles/r1_traffic.json
 
