@@ -46,9 +46,8 @@ struct Vec1x1Tile {
 
 // split-C through DSMEM (see cluster_reduce_tile in conv_kernel.cuh): park the
 // accumulator tile [BM][BP] in this CTA's shared memory, then reduce.
-template <int BM, int BP, int NT>
-__device__ __forceinline__ void vec_cluster_epilogue(const KParams &p, const float2 (&acc)[4][8], float *tile,
-                                                     int m0, int q0, int wrow, int xcol) {
+template <int BM, int BP>
+__device__ __forceinline__ void vec_park_tile(const float2 (&acc)[4][8], float *tile, int wrow, int xcol) {
   __syncthreads();  // every warp is done with the pipeline stages the tile overwrites
 #pragma unroll
   for (int g = 0; g < 2; g++)
@@ -64,6 +63,12 @@ __device__ __forceinline__ void vec_cluster_epilogue(const KParams &p, const flo
       const int row = wrow + (r & 3) + (r >> 2) * 16;
       *reinterpret_cast<float4 *>(tile + row * BP + xcol + 32 * g) = v;
     }
+}
+
+template <int BM, int BP, int NT>
+__device__ __forceinline__ void vec_cluster_epilogue(const KParams &p, const float2 (&acc)[4][8], float *tile,
+                                                     int m0, int q0, int wrow, int xcol) {
+  vec_park_tile<BM, BP>(acc, tile, wrow, xcol);
   cluster_reduce_tile<BM, BP, NT>(p, tile, m0, q0);
 }
 
@@ -220,27 +225,14 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC>::NT, Vec1x1Tile<WM, WP,
     }
     return;
   }
-  // epilogue: 4 consecutive pixels per (channel, group) -> one 16-byte store
-  // (VEC), or four scalar stores that may straddle two images
+  // epilogue: VEC -> one 16-byte store per 4 consecutive pixels of a channel;
+  // !VEC (planes with H*W % 4 != 0, strided) -> the tile goes through shared
+  // memory and every warp stores runs of consecutive pixels
   float *dst = p.splits > 1 ? p.partials + (long long)split * p.part_stride : p.y;
-  if (!VEC) {
-#pragma unroll
-    for (int g = 0; g < 2; g++) {
-#pragma unroll
-      for (int e = 0; e < 4; e++) {
-        const int q = q0 + xcol + 32 * g + e;
-        if (q >= p.Q) continue;
-        const int n = q / hw;
-        const long long base = (long long)n * p.M * hw + (q - n * hw);
-#pragma unroll
-        for (int r = 0; r < 8; r++) {
-          const int m = m0 + wrow + (r & 3) + (r >> 2) * 16;
-          if (m >= p.M) continue;
-          const float2 a = acc[r >> 1][4 * g + e];
-          dst[base + (long long)m * hw] = (r & 1) ? a.y : a.x;
-        }
-      }
-    }
+  if (!VEC) {  // transpose through shared memory, then coalesced per-pixel stores
+    vec_park_tile<BM, BP>(acc, smem, wrow, xcol);
+    __syncthreads();
+    store_tile_coalesced<BM, BP, NT>(p, smem, dst, m0, q0, 0, BM * BP);
     if (p.trace && tid == 0) {
       const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
       p.trace[5 * cta + 4] = global_ns();

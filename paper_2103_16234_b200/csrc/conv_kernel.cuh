@@ -129,8 +129,29 @@ __device__ __forceinline__ float4 ld_dsmem_f4(unsigned local_addr, unsigned rank
   return v;
 }
 
+// Store elements [lo, hi) of a shared-memory tile [BM][BP] (row = output
+// channel, column = output pixel q0 + col) to `dst` (y layout): consecutive
+// threads take consecutive pixels, so a warp writes one contiguous run per
+// image (coalesced for any H*W, unlike per-thread register tiles).
 template <int BM, int BP, int NT>
-__device__ __forceinline__ void cluster_reduce_tile(const KParams &p, const float *tile, int m0, int q0) {
+__device__ __forceinline__ void store_tile_coalesced(const KParams &p, const float *tile, float *dst, int m0, int q0,
+                                                     int lo, int hi) {
+  const int hw = p.HoWo;
+  const int n0 = q0 / hw;
+  const int r0 = q0 - n0 * hw;
+  for (int i = lo + (int)threadIdx.x; i < hi; i += NT) {
+    const int row = i / BP;
+    const int col = i - row * BP;
+    const int m = m0 + row;
+    if (m >= p.M || q0 + col >= p.Q) continue;
+    const int rel = r0 + col;  // < hw + BP < 2^20
+    const int dn = fdiv(rel, p.mHoWo);
+    dst[(long long)(n0 + dn) * p.M * hw + (long long)m * hw + (rel - dn * hw)] = tile[i];
+  }
+}
+
+template <int BM, int BP, int NT>
+__device__ __forceinline__ void cluster_reduce_tile(const KParams &p, float *tile, int m0, int q0) {
   cluster_barrier();
   constexpr int F4 = BM * BP / 4;
   const int S = p.splits;
@@ -158,15 +179,13 @@ __device__ __forceinline__ void cluster_reduce_tile(const KParams &p, const floa
       const int n = q / hw;
       *reinterpret_cast<float4 *>(p.y + (long long)n * p.M * hw + (long long)m * hw + (q - n * hw)) = a;
     } else {
-      const float av[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-      for (int e = 0; e < 4; e++) {
-        const int qe = q + e;
-        if (qe >= p.Q) break;
-        const int n = qe / hw;
-        p.y[(long long)n * p.M * hw + (long long)m * hw + (qe - n * hw)] = av[e];
-      }
+      // slice i of this CTA's own tile is read by this CTA only: park the sum there
+      *reinterpret_cast<float4 *>(tile + 4 * i) = a;
     }
+  }
+  if (!vec) {
+    __syncthreads();
+    store_tile_coalesced<BM, BP, NT>(p, tile, p.y, m0, q0, 4 * lo, 4 * hi);
   }
   cluster_barrier();  // keep this CTA's tile alive until every rank has read it
 }

@@ -206,7 +206,8 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
       tc.splits = (int)cdiv(nchunks, tc.chunks_per_split);
       if (tc.splits != sp && forced_splits <= 0) continue;
       tc.stages = f.stages;
-      const long long smem = 4LL * f.stages * ((long long)f.bc * f.bp + (long long)f.bc * (f.bm + 4));
+      long long smem = 4LL * f.stages * ((long long)f.bc * f.bp + (long long)f.bc * (f.bm + 4));
+      if (f.kind == 2) smem = std::max(smem, 4LL * f.bm * f.bp);  // epilogue transposes the tile in smem
       if (smem > 226 * 1024) return false;
       tc.smem_bytes = (int)smem;
       const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
