@@ -464,3 +464,27 @@ def test_bench_dominant_kernel_roofline_fields(tmp_path, monkeypatch):
     assert abs(d["achieved_tflops"] - sum(cfgs[i].flops for i in idx) / (sum(ms[i] for i in idx) * 1e-3) / 1e12) < 1e-9
     assert d["traffic"] == round(sum(1000 + i for i in idx) / len(idx)) and d["traffic_source"]
     assert bench.dominant_kernel(cfgs, layers, ms, "c3")["traffic"] is None  # no capture for that workload
+
+
+def test_bench_reference_arm_contract_line():
+    """`bench.py --impl reference` runs on the host (no GPU) and prints one JSON
+    line with the contract keys, its own cpu_baseline and a zero-copy e2e."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "c1", "--steps", "1",
+                        "--warmup", "3"], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["steps"] == 1 and d["warmup"] == 3 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    assert "workload" in d["config"] and "model" not in d["config"]
