@@ -242,3 +242,33 @@ def test_harness_cli_validate_and_run(tmp_path, capsys):
     assert H.main(["run", "--algos", "fused,tf32", "--batches", "2", "--repeats", "2", "--baseline", "fused",
                    "--out", str(rep)]) == 0
     assert rep.read_text().count("\n") == len(pk.preset_configs()) * 2 + 1
+
+
+def test_bench_line_contract_on_gpu():
+    """bench.py (our arm) prints one JSON line with every contract key: device
+    value, e2e through the C ABI with host buffers, the dominant-kernel
+    roofline, clocks sampled during the timed region, our kernel launches."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "bench.py", "--workload", "c1", "--steps", "3", "--warmup", "3",
+                        "--e2e-steps", "1", "--no-cpu-baseline"], cwd=root, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1 and d["value"] > 0
+    rf = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= rf.keys()
+    assert 0 < rf["frac"] < 1.5 and abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-3
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
+    assert d["gpu_launches"] >= d["steps"]
