@@ -9,6 +9,7 @@ engine from the reference package.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -16,6 +17,8 @@ from .errors import (ConvKitError, DeviceError, InvalidConfig, InvalidPlan, Shap
                      Unsupported, WorkspaceExceeded)
 
 LIB_PATH = Path(__file__).resolve().parent / "libb2conv.so"
+if os.environ.get("B2C_LIB_VARIANT"):  # development A/B of two in-tree builds (libb2conv_<variant>.so)
+    LIB_PATH = LIB_PATH.with_name(f"libb2conv_{os.environ['B2C_LIB_VARIANT']}.so")
 
 OK, UNSUPPORTED, SHAPE_MISMATCH, INVALID_PLAN, WORKSPACE_EXCEEDED, INVALID_CONFIG, CUDA_ERROR, INVALID_ARGUMENT = range(8)
 ENGINE_FUSED, ENGINE_TWOSTAGE, ENGINE_TF32X3, ENGINE_TF32 = 0, 1, 2, 3
