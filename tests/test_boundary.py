@@ -488,3 +488,33 @@ def test_bench_reference_arm_contract_line():
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert "workload" in d["config"] and "model" not in d["config"]
+
+
+def test_every_shipped_tuned_plan_is_what_the_planner_returns():
+    """tuned_plans.json (measured on B200, registered at import) must be live:
+    for every entry the planner's automatic choice for that exact shape is the
+    recorded plan (a stale or rejected entry would silently fall back to the
+    cost model)."""
+    import json
+
+    from paper_2103_16234_b200 import _native as nat
+
+    entries = json.loads(nat.TUNED_PATH.read_text())["plans"]
+    assert len(entries) > 200
+    keys = ("n", "c", "h", "w", "m", "hf", "wf", "stride", "pad_h", "pad_w")
+    for e in entries:
+        cfg = pk.ConvConfig("tuned", **dict(zip(keys, e["desc"])))
+        L = pk.ConvLayer(cfg, e["engine"])
+        if e["engine"] == "fused":
+            assert L.family.replace("_dsm", "") == e["family"], e["layer"]
+            if e.get("splits", 0) > 0:
+                assert L.splits == e["splits"], e["layer"]
+            if L.splits > 1 and e.get("reduce", 0) > 0:
+                assert L.reduce == e["reduce"], e["layer"]
+        else:
+            t = L._tc
+            assert (t.mode == 2) == (e["mode"] == 2), e["layer"]
+            if e["nf"] > 0:
+                assert t.filters_per_tile == e["nf"], e["layer"]
+            if e["splits"] > 0:
+                assert t.splits == e["splits"], e["layer"]
