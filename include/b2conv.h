@@ -135,8 +135,10 @@ typedef struct {
                                padded-input halo per channel block, taps are
                                descriptor offsets)                            */
   int32_t halo_positions;   /* out: staged positions per tile (mode 2)        */
-  int32_t m_halves;         /* out: 128-pixel UMMA M halves per tile (mode 2:
-                               1 or 2, sharing each filter tile)              */
+  int32_t m_halves;         /* in/out: 128-pixel UMMA M slices per tile (mode 2:
+                               1, 2 or 4, sharing each filter tile); on input
+                               0 = planner's choice, 1/2/4 force it for halo
+                               plans                                          */
   int32_t bf16_corrections; /* out: 3xTF32 correction products run as bf16
                                MMAs (K=16, twice the tf32 rate)               */
   int32_t k_packed;         /* out: mode 1 with few input channels: the
@@ -210,14 +212,15 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
 b2c_status b2c_conv2d_forward_tc(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
                                  int64_t workspace_size, int32_t engine, const b2c_tc_plan *tiles, void *stream);
 /* The tensor-core planner's choice for d (B2C_UNSUPPORTED if not covered).
- * out->filters_per_tile / out->splits > 0 on entry are forced. */
+ * out->filters_per_tile / out->splits / out->mode / out->m_halves > 0 on entry
+ * are forced. */
 b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_plan *out);
 
 /* Register a measured tensor-core plan (tools/autotune.py) for an exact shape:
- * the planner then uses (mode, filters_per_tile, splits) for it.  The Python
- * package registers paper_2103_16234_b200/tuned_plans.json at import. */
+ * the planner then uses (mode, filters_per_tile, splits, m_halves) for it.  The
+ * Python package registers paper_2103_16234_b200/tuned_plans.json at import. */
 b2c_status b2c_register_tuned_tc_plan(const b2c_conv_desc *d, int32_t engine, int32_t mode, int32_t filters_per_tile,
-                                      int32_t splits);
+                                      int32_t splits, int32_t m_halves);
 
 /* twostage.conv_twostage (twostage.py:208-239): preconditions in the
  * reference's order, then stage 1 (+ stage 2 unless 1x1) with the reference's

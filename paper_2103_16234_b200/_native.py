@@ -89,7 +89,7 @@ SIGNATURES = {
                                              ctypes.c_int32, _P(TcPlanC), ctypes.c_void_p]),
     "b2c_tc_select_tiles": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, _P(TcPlanC)]),
     "b2c_register_tuned_tc_plan": (ctypes.c_int, [_P(ConvDesc), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
-                                                  ctypes.c_int32]),
+                                                  ctypes.c_int32, ctypes.c_int32]),
     "b2c_conv_twostage": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _fp, ctypes.c_int64, _P(LaunchPlanC),
                                          _P(DeviceModelC), ctypes.c_int64, ctypes.c_void_p, _P(RunStatsC)]),
     "b2c_stage1_scalar_prods": (ctypes.c_int, [_P(ConvDesc), _fp, _fp, _fp, _P(LaunchPlanC), _P(DeviceModelC),
@@ -153,7 +153,7 @@ def _register_tuned(l) -> None:
         if e.get("engine") in ("tf32x3", "tf32"):
             d = ConvDesc(*[int(v) for v in e["desc"]])
             l.b2c_register_tuned_tc_plan(ctypes.byref(d), ENGINES[e["engine"]], int(e["mode"]), int(e["nf"]),
-                                         int(e["splits"]))
+                                         int(e["splits"]), int(e.get("mh", 0)))
             continue
         if e.get("family") not in names:
             continue

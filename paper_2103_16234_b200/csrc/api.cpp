@@ -437,15 +437,17 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
 
 namespace {
 b2c_status tc_plan_of(const b2c_conv_desc *d, const b2c::Geom &g, int32_t engine, int forced_nf, int forced_splits,
-                      b2c::TcPlan *pl, int forced_mode = 0) {
+                      b2c::TcPlan *pl, int forced_mode = 0, int forced_mh = 0) {
   if (engine != B2C_ENGINE_TF32X3 && engine != B2C_ENGINE_TF32)
     return fail(B2C_INVALID_ARGUMENT, "engine %d is not a tensor-core engine", engine);
   if (forced_nf > 0 && (forced_nf % 16 != 0 || forced_nf > 256))
     return fail(B2C_INVALID_PLAN, "filters_per_tile must be a multiple of 16 in [16, 256], got %d", forced_nf);
   if (forced_splits < 0 || forced_splits > 64) return fail(B2C_INVALID_PLAN, "splits must be in [0, 64], got %d", forced_splits);
   if (forced_mode < 0 || forced_mode > 2) return fail(B2C_INVALID_PLAN, "mode must be 0, 1 or 2, got %d", forced_mode);
-  if (!b2c::plan_tc(g, engine == B2C_ENGINE_TF32X3 ? 3 : 1, forced_nf, 0, forced_splits, pl, forced_mode)) {
-    if (forced_splits > 0 || forced_nf > 0 || forced_mode > 0)
+  if (forced_mh != 0 && forced_mh != 1 && forced_mh != 2 && forced_mh != 4)
+    return fail(B2C_INVALID_PLAN, "m_halves must be 0, 1, 2 or 4, got %d", forced_mh);
+  if (!b2c::plan_tc(g, engine == B2C_ENGINE_TF32X3 ? 3 : 1, forced_nf, 0, forced_splits, pl, forced_mode, forced_mh)) {
+    if (forced_splits > 0 || forced_nf > 0 || forced_mode > 0 || forced_mh > 0)
       return fail(B2C_INVALID_PLAN, "forced tensor-core tile (filters %d, splits %d) cannot run this layer", forced_nf,
                   forced_splits);
     return fail(B2C_UNSUPPORTED, "layer too large for the tensor-core engine's 32-bit per-image offsets");
@@ -462,7 +464,8 @@ b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_pl
   b2c::Geom g = geom_of(d);
   if ((st = check_sizes(g)) != B2C_OK) return st;
   b2c::TcPlan pl;
-  if ((st = tc_plan_of(d, g, engine, out->filters_per_tile, out->splits, &pl, out->mode)) != B2C_OK) return st;
+  if ((st = tc_plan_of(d, g, engine, out->filters_per_tile, out->splits, &pl, out->mode, out->m_halves)) != B2C_OK)
+    return st;
   out->pixels_per_chunk = pl.xb;
   out->filters_per_tile = pl.nf;
   out->filter_tiles = pl.mtiles;
@@ -483,13 +486,13 @@ b2c_status b2c_tc_select_tiles(const b2c_conv_desc *d, int32_t engine, b2c_tc_pl
 }
 
 b2c_status b2c_register_tuned_tc_plan(const b2c_conv_desc *d, int32_t engine, int32_t mode, int32_t filters_per_tile,
-                                      int32_t splits) {
+                                      int32_t splits, int32_t m_halves) {
   b2c_status st = check_config(d, nullptr);
   if (st != B2C_OK) return st;
   b2c::Geom g = geom_of(d);
   b2c::TcPlan pl;
-  if ((st = tc_plan_of(d, g, engine, filters_per_tile, splits, &pl, mode)) != B2C_OK) return st;  // must be runnable
-  b2c::register_tuned_tc(g, engine == B2C_ENGINE_TF32X3 ? 3 : 1, mode, filters_per_tile, splits);
+  if ((st = tc_plan_of(d, g, engine, filters_per_tile, splits, &pl, mode, m_halves)) != B2C_OK) return st;  // runnable
+  b2c::register_tuned_tc(g, engine == B2C_ENGINE_TF32X3 ? 3 : 1, mode, filters_per_tile, splits, m_halves);
   return B2C_OK;
 }
 
@@ -502,7 +505,7 @@ b2c_status b2c_conv2d_forward_tc(const b2c_conv_desc *d, const float *x, const f
   if ((st = check_sizes(g)) != B2C_OK) return st;
   b2c::TcPlan pl;
   if ((st = tc_plan_of(d, g, engine, tiles ? tiles->filters_per_tile : 0, tiles ? tiles->splits : 0, &pl,
-                       tiles ? tiles->mode : 0)) != B2C_OK)
+                       tiles ? tiles->mode : 0, tiles ? tiles->m_halves : 0)) != B2C_OK)
     return st;
   if (!workspace || workspace_size < b2c::tc_workspace_bytes(g, pl))
     return fail(B2C_INVALID_ARGUMENT, "tensor-core engine needs a %lld-byte filter workspace, %lld provided",

@@ -86,23 +86,23 @@ struct TcKeyHash {
     return h;
   }
 };
-std::unordered_map<TcKey, std::array<int, 3>, TcKeyHash> g_tc_tuned;
+std::unordered_map<TcKey, std::array<int, 4>, TcKeyHash> g_tc_tuned;
 std::mutex g_tc_tuned_mu;
 TcKey tc_key(const Geom &g, int passes) {
   return TcKey{{g.N, g.C, g.H, g.W, g.M, g.HF, g.WF, g.S, g.PH, g.PW, passes}};
 }
 }  // namespace
 
-void register_tuned_tc(const Geom &g, int passes, int mode, int nf, int splits) {
+void register_tuned_tc(const Geom &g, int passes, int mode, int nf, int splits, int mh) {
   std::lock_guard<std::mutex> lk(g_tc_tuned_mu);
-  g_tc_tuned[tc_key(g, passes)] = {mode, nf, splits};
+  g_tc_tuned[tc_key(g, passes)] = {mode, nf, splits, mh};
 }
 
 bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced_splits, TcPlan *out,
-             int forced_mode) {
+             int forced_mode, int forced_mh) {
   if (!tc_supported(g)) return false;
-  if (forced_nf <= 0 && forced_splits <= 0 && forced_mode <= 0 && forced_xb <= 0) {
-    std::array<int, 3> t{0, 0, 0};
+  if (forced_nf <= 0 && forced_splits <= 0 && forced_mode <= 0 && forced_xb <= 0 && forced_mh <= 0) {
+    std::array<int, 4> t{0, 0, 0, 0};
     bool hit = false;
     {
       std::lock_guard<std::mutex> lk(g_tc_tuned_mu);
@@ -112,7 +112,7 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
         hit = true;
       }
     }
-    if (hit && plan_tc(g, passes, t[1], 0, t[2], out, t[0])) return true;
+    if (hit && plan_tc(g, passes, t[1], 0, t[2], out, t[0], t[3])) return true;
   }
   const bool flat = tc_flat(g);
   const int wo = flat ? g.HoWo : g.Wo;
@@ -158,6 +158,7 @@ bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced
   for (int mode = 1; mode <= 4; mode++) {
     const int mh = mode == 4 ? 4 : mode == 3 ? 2 : 1;
     if (forced_mode > 0 && (mode == 1) != (forced_mode == 1)) continue;
+    if (forced_mh > 0 && mode >= 2 && mh != forced_mh) continue;  // halo M slices forced (1, 2 or 4)
     if (mode >= 2 && !halo_ok) continue;
     const long long halo = (tc::TILE_P * mh + (g.HF - 1) * Wp + (g.WF - 1) + 7) / 8 * 8;
     const long long ptiles = mode == 1 ? cdiv(nchunks, tc::TILE_P / 32) : cdiv((long long)g.N * Hp * Wp, tc::TILE_P * mh);

@@ -51,9 +51,9 @@ bool tc_supported(const Geom &g);
 bool tc_flat(const Geom &g);
 long long tc_workspace_bytes(const Geom &g, const TcPlan &pl);
 bool plan_tc(const Geom &g, int passes, int forced_nf, int forced_xb, int forced_splits, TcPlan *out,
-             int forced_mode = 0);
+             int forced_mode = 0, int forced_mh = 0);
 long long tc_filter_bytes(const Geom &g, const TcPlan &pl);
-void register_tuned_tc(const Geom &g, int passes, int mode, int nf, int splits);
+void register_tuned_tc(const Geom &g, int passes, int mode, int nf, int splits, int mh = 0);
 cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const float *w, float *y, void *workspace,
                       long long ws_bytes, cudaStream_t stream);
 

@@ -57,7 +57,7 @@ class ConvLayer:
     """A resolved forward convolution for one configuration."""
 
     def __init__(self, cfg: ConvConfig, engine: str = "fused", family: int = -1, splits: int = 0,
-                 filters_per_tile: int = 0, tc_mode: int = 0, reduce: int = 0):
+                 filters_per_tile: int = 0, tc_mode: int = 0, reduce: int = 0, tc_m_halves: int = 0):
         if engine not in nat.ENGINES:
             raise ValueError(f"unknown engine {engine!r}")
         if engine == "twostage" and cfg.stride != 1:
@@ -77,6 +77,7 @@ class ConvLayer:
             self._tc.filters_per_tile = int(filters_per_tile)
             self._tc.splits = int(splits)
             self._tc.mode = int(tc_mode)
+            self._tc.m_halves = int(tc_m_halves)  # halo plans: 128-pixel M slices per tile (0 = planner)
             nat.check(self._lib.b2c_tc_select_tiles(ctypes.byref(self._desc), self._engine_id, ctypes.byref(self._tc)))
         else:
             e = nat.ENGINE_TWOSTAGE if engine == "twostage" else nat.ENGINE_FUSED

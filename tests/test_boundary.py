@@ -518,3 +518,28 @@ def test_every_shipped_tuned_plan_is_what_the_planner_returns():
                 assert t.filters_per_tile == e["nf"], e["layer"]
             if e["splits"] > 0:
                 assert t.splits == e["splits"], e["layer"]
+
+
+def test_tc_forced_m_halves():
+    """b2c_tc_plan.m_halves on input forces the halo plan's M slices (1/2/4);
+    other values are rejected; gather plans ignore it."""
+    import ctypes
+
+    from paper_2103_16234_b200 import _native as nat
+
+    cfg = pk.ConvConfig("mh", n=8, c=64, h=28, w=28, m=64, hf=3, wf=3, pad_h=1, pad_w=1)
+    lib = nat.lib()
+    for mh in (1, 2, 4):
+        p = nat.TcPlanC()
+        p.mode, p.m_halves = 2, mh
+        assert lib.b2c_tc_select_tiles(ctypes.byref(nat.desc(cfg)), nat.ENGINE_TF32X3, ctypes.byref(p)) == nat.OK
+        assert p.mode == 2 and p.m_halves == mh
+        L = pk.ConvLayer(cfg, "tf32x3", tc_mode=2, tc_m_halves=mh)
+        assert L._tc.m_halves == mh
+    p = nat.TcPlanC()
+    p.m_halves = 3
+    assert lib.b2c_tc_select_tiles(ctypes.byref(nat.desc(cfg)), nat.ENGINE_TF32X3, ctypes.byref(p)) != nat.OK
+    p = nat.TcPlanC()
+    p.mode, p.m_halves = 1, 4
+    assert lib.b2c_tc_select_tiles(ctypes.byref(nat.desc(cfg)), nat.ENGINE_TF32X3, ctypes.byref(p)) == nat.OK
+    assert p.mode == 1

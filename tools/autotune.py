@@ -49,27 +49,29 @@ def tune_tc(cfg, eng, x, w, label, desc):
     auto = ConvLayer(cfg, eng)
     y = torch.empty(auto.output_shape(), device="cuda")
     t_auto = time_layer(auto, x, w, y)
-    best = (t_auto, auto._tc.mode, 0, 0, auto.family)
-    seen = {auto.family}
-    for mode in (1, 2):
+    best = (t_auto, auto._tc.mode, 0, 0, auto.family, 0)
+    seen = {(auto.family, auto._tc.m_halves)}
+    for mode, mh in ((1, 0), (2, 1), (2, 2), (2, 4)):
         for nf in (0, 32, 64, 96, 128, 192, 256):
             for sp in (0, 1, 2, 3, 4, 6, 8, 12):
                 try:
-                    L = ConvLayer(cfg, eng, tc_mode=mode, filters_per_tile=nf, splits=sp)
+                    L = ConvLayer(cfg, eng, tc_mode=mode, filters_per_tile=nf, splits=sp, tc_m_halves=mh)
                 except Exception:  # noqa: BLE001
                     continue
-                if L.family in seen or (eng == "tf32x3" and not tc_accurate(cfg, L)):
+                key = (L.family, L._tc.m_halves)
+                if key in seen or (eng == "tf32x3" and not tc_accurate(cfg, L)):
                     continue
-                seen.add(L.family)
+                seen.add(key)
                 t = time_layer(L, x, w, y)
                 if t < best[0]:
-                    best = (t, L._tc.mode, L._tc.filters_per_tile, L._tc.splits, L.family)
+                    best = (t, L._tc.mode, L._tc.filters_per_tile, L._tc.splits, L.family, L._tc.m_halves)
     del y
     if best[2] == 0:
         return {"layer": label, "desc": desc, "engine": eng, "mode": best[1], "nf": 0, "splits": 0,
                 "plan": best[4], "us": round(best[0], 2), "model_us": round(t_auto, 2)}
     return {"layer": label, "desc": desc, "engine": eng, "mode": best[1], "nf": best[2], "splits": best[3],
-            "plan": best[4], "us": round(best[0], 2), "model_us": round(t_auto, 2)}
+            "mh": best[5] if best[1] == 2 else 0, "plan": best[4], "us": round(best[0], 2),
+            "model_us": round(t_auto, 2)}
 
 
 def main():
