@@ -9,6 +9,7 @@
 #include <cstring>
 #include <array>
 #include <mutex>
+#include <set>
 #include <unordered_map>
 #include <cstdio>
 
@@ -340,11 +341,25 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   if (const char *m = std::getenv("B2C_TC_MODE")) p.mode = std::atoi(m);
 
   const void *kern = tc_kernel(kpasses, pl.halo > 0, pl.mh);
+  // once per (kernel, device): allow the full opt-in shared memory, so launches
+  // carry no attribute calls
   static std::mutex mu;
+  static std::set<std::pair<const void *, int>> attr_done;
   {
+    int dev = 0;
+    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_bytes);
-    if (e != cudaSuccess) return e;
+    if (!attr_done.count({kern, dev})) {
+      int optin = 0;
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncAttributes fa;
+      cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               std::max(pl.smem_bytes, optin - (int)fa.sharedSizeBytes));
+      if (e != cudaSuccess) return e;
+      attr_done.insert({kern, dev});
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(pl.grid / pl.splits), (unsigned)pl.splits);
