@@ -190,13 +190,15 @@ b2c_status b2c_register_tuned_plan(const b2c_conv_desc *d, int32_t engine, int32
 /* Fused direct convolution (any stride >= 1, any padding).  Replaces the
  * compute of twostage.conv_twostage (twostage.py:208-239) and
  * reference.conv_naive (reference.py:58-83) for device-resident tensors.
- * `tiles` may be NULL (planner's choice) or carry a forced family / split.
- * Layers with too few output tiles for 148 SMs are split over channel ranges
- * (split-C): each range writes a partial plane into `workspace`
- * (tiles.workspace_bytes from b2c_select_tiles, splits*N*M*Ho*Wo*4 bytes) and
- * a second launch adds the planes in ascending range order.  With no (or too
- * small a) workspace the planner picks an unsplit plan.  Per output, the
- * summation order is a function of (c, hf, wf, splits) only. */
+ * `tiles` may be NULL (planner's choice) or carry a forced family / split /
+ * reduction mode.  Layers with too few output tiles for 148 SMs are split over
+ * channel ranges (split-C), reduced either (reduce = 1) through partial planes
+ * in `workspace` (tiles.workspace_bytes from b2c_select_tiles,
+ * splits*N*M*Ho*Wo*4 bytes) and a second launch that adds them in ascending
+ * range order, or (reduce = 2) inside a thread-block cluster through DSMEM in
+ * the same order (one launch).  With no (or too small a) workspace the planner
+ * picks an unsplit plan.  Per output, the summation order is a function of
+ * (c, hf, wf, splits) only: both reductions give bitwise-identical results. */
 b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
                               int64_t workspace_size, const b2c_tile_plan *tiles, void *stream);
 
