@@ -23,7 +23,7 @@
 //
 // Tiling (B200-first, not the paper's one-filter-row-per-block mapping):
 //   CTA = BM output channels x BP flattened output pixels (n, y, x order).
-//   Thread = RM (16, or 8 for the r8 families) channels x RP=4 pixels; a thread's pixels are strided by
+//   Thread = RM=16 channels x RP=4 pixels; a thread's pixels are strided by
 //   NTP so a warp's lanes touch consecutive pixels (conflict-free shared loads,
 //   coalesced stores), and all lanes of a warp share their 16 channels (weight
 //   loads are warp-wide broadcasts, LDS.128).
@@ -191,9 +191,9 @@ __device__ __forceinline__ void cluster_reduce_tile(const KParams &p, float *til
 }
 
 // HF_T/WF_T/S_T == 0 -> taken from the runtime parameters (generic family).
-template <int HF_T, int WF_T, int S_T, int BM, int BP, int BC, bool STRICT, int RM_T = 16>
+template <int HF_T, int WF_T, int S_T, int BM, int BP, int BC, bool STRICT>
 struct ConvTile {
-  static constexpr int RM = RM_T;  // output channels per thread (16; 8 = lighter tile, twice the warps)
+  static constexpr int RM = 16;
   static constexpr int RP = 4;
   static constexpr int NTP = BP / RP;
   static constexpr int NMG = BM / RM;
@@ -201,15 +201,15 @@ struct ConvTile {
   static constexpr int WS = BM + 4;  // weight row stride: keeps LDS.128 alignment, spreads banks
   // target 16 resident warps per SM at <= 128 registers per thread
   static constexpr int MIN_BLOCKS = NT >= 512 ? 1 : 512 / NT;
-  static_assert(BM % RM == 0 && RM % 4 == 0, "BM must be a multiple of RM (a multiple of 4)");
+  static_assert(BM % RM == 0, "BM must be a multiple of 16");
   static_assert(NTP % 32 == 0, "a warp must share one channel group");
 };
 
-template <int HF_T, int WF_T, int S_T, int BM, int BP, int BC, bool STRICT, int RM_T = 16>
-__global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT, RM_T>::NT,
-                                  ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT, RM_T>::MIN_BLOCKS)
+template <int HF_T, int WF_T, int S_T, int BM, int BP, int BC, bool STRICT>
+__global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>::NT,
+                                  ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>::MIN_BLOCKS)
     conv_direct_kernel(const KParams p) {
-  using T = ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT, RM_T>;
+  using T = ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>;
   constexpr int RM = T::RM, RP = T::RP, NTP = T::NTP, NT = T::NT, WS = T::WS;
   const int hf = HF_T ? HF_T : p.HF;
   const int wf = WF_T ? WF_T : p.WF;

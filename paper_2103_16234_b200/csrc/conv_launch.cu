@@ -46,14 +46,6 @@ struct Family {
         ConvTile<HF, WF, S, BM, BP, BC, STRICT>::MIN_BLOCKS, 0, 2                                          \
   }
 
-// lighter register tile: RM output channels per thread instead of 16
-#define B2C_FAMILY_RM(NAME, HF, WF, S, BM, BP, BC, RM)                                                     \
-  Family {                                                                                                 \
-    NAME, HF, WF, S, BM, BP, BC, false, ConvTile<HF, WF, S, BM, BP, BC, false, RM>::NT,                    \
-        reinterpret_cast<const void *>(&conv_direct_kernel<HF, WF, S, BM, BP, BC, false, RM>),             \
-        ConvTile<HF, WF, S, BM, BP, BC, false, RM>::MIN_BLOCKS, 0, 2                                       \
-  }
-
 #define B2C_VEC1X1(NAME, WM, WP, BC)                                                                       \
   Family {                                                                                                 \
     NAME, 1, 1, 1, Vec1x1Tile<WM, WP, BC>::BM, Vec1x1Tile<WM, WP, BC>::BP, BC, false,                      \
@@ -79,8 +71,6 @@ const Family kFamilies[] = {
     B2C_FAMILY("fused_3x3s1_m32", 3, 3, 1, 32, 256, 8, false),
     B2C_FAMILY("fused_3x3s1_m32p128", 3, 3, 1, 32, 128, 8, false),  // small tiles: latency-bound batch-1 layers
     B2C_FAMILY("fused_3x3s1_m64p128", 3, 3, 1, 64, 128, 8, false),
-    B2C_FAMILY_RM("fused_3x3s1_m64r8", 3, 3, 1, 64, 256, 8, 8),  // 8 channels per thread: batch-1 layers
-    B2C_FAMILY_RM("fused_3x3s1_m32r8", 3, 3, 1, 32, 256, 8, 8),
     B2C_FAMILY("fused_3x3s1_m64", 3, 3, 1, 64, 256, 8, false),
     B2C_FAMILY("fused_3x3s1_m128", 3, 3, 1, 128, 256, 8, false),
     B2C_FAMILY("fused_3x3s2_m64", 3, 3, 2, 64, 256, 8, false),
