@@ -14,7 +14,6 @@
 from __future__ import annotations
 
 import hashlib
-from pathlib import Path
 
 import numpy as np
 import pytest
@@ -23,7 +22,6 @@ from conftest import cfg_from
 
 import paper_2103_16234_b200 as pk
 
-ROOT = Path(__file__).resolve().parents[1]
 
 pytestmark = pytest.mark.gpu
 
