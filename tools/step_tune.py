@@ -48,6 +48,9 @@ def main():
     groups = W.schedule(a.workload, cfgs)
     xs, ws, ys = bench.make_operands(cfgs, dev, 0)
     targs = SimpleNamespace(steps=a.steps, warmup=3)
+    # the tuned-plan registry is keyed by shape, so layers with identical shapes
+    # (e.g. GoogLeNet 3b-1x1 and 3b-3x3red) must share one plan
+    twins = {i: [j for j, d in enumerate(cfgs) if d.as_tuple() == c.as_tuple()] for i, c in enumerate(cfgs)}
     plans = []
     for cfg in cfgs:
         L = ConvLayer(cfg)
@@ -86,13 +89,15 @@ def main():
                 if L.splits != s:
                     continue
                 trial = list(plans)
-                trial[i] = (f, s, L.reduce)
+                for j in twins[i]:
+                    trial[j] = (f, s, L.reduce)
                 t = measure(trial)
                 if t < best[0] * 0.996:
                     best = (t, (f, s, L.reduce))
             if best[1] != plans[i]:
                 trial = list(plans)
-                trial[i] = best[1]
+                for j in twins[i]:
+                    trial[j] = best[1]
                 # confirm against a fresh measurement of the incumbent
                 t_new, t_old = measure(trial, 3), measure(plans, 3)
                 if t_new < t_old * 0.997:
