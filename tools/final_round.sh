@@ -17,7 +17,7 @@ for wl in c1 c3 c4 c5; do
   timeout 900 python bench.py --workload $wl --steps 10 --warmup 3 --e2e-steps 1 --no-cpu-baseline > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-  python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
+  python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline --tc-engine none > $OUT/ncu_bench.log 2>&1
 # one --set full capture of the top C2 layer's kernel and of the C1 kernel (plans as shipped)
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"conv" -c 1 --launch-skip 2 \
   -o $OUT/c2_4e1x1 python tools/prof_layer.py c2 32 4e-1x1 > $OUT/ncu_c2.log 2>&1
