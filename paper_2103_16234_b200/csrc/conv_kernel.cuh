@@ -68,7 +68,7 @@ struct KParams {
   long long y_tap_stride;  // stage 1: elements between partial planes of consecutive k
   int strict_tap_major;    // stage 1: blockIdx.z selects the filter row
   unsigned long long *trace;  // optional per-CTA (smid, t_start, t_tables, t_loop, t_end) records
-  unsigned long long mRS, mHp, mHoWo, mWo;  // exact division magics: floor(2^32/d) + 1
+  unsigned long long mRS, mHp, mHoWo, mWo;  // exact division magics: floor(2^44/d) + 1 (see fdiv)
   int pdl;                    // launched with programmatic dependent launch
   int cluster;                // split-C partials reduced through DSMEM: the splits of a tile form one cluster
 };
@@ -78,9 +78,18 @@ __device__ __forceinline__ unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// floor(x / d) for 0 <= x < 2^20 via a host-computed magic m = floor(2^32/d) + 1
+// floor(x / d) via a host-computed magic m = floor(2^44/d) + 1 (fdiv_magic).
+// Exact for 0 <= x < 2^20 and 1 <= d < 2^24: m = 2^44/d + e with 0 < e <= 1,
+// so x*m/2^44 = x/d + x*e/2^44 with x*e/2^44 < 2^-24 < 1/d, which never
+// carries past the next integer; x*m < 2^20 * (2^44 + 1) fits 64 bits.  The
+// planner keeps every divided quantity below 2^20 (fdiv_range_ok).
+constexpr int kFdivShift = 44;
+constexpr long long kFdivLimit = 1LL << 20;
+__host__ __device__ __forceinline__ unsigned long long fdiv_magic(int d) {
+  return ((1ULL << kFdivShift) / (unsigned long long)d) + 1ULL;
+}
 __device__ __forceinline__ int fdiv(int x, unsigned long long m) {
-  return (int)(((unsigned long long)(unsigned)x * m) >> 32);
+  return (int)(((unsigned long long)(unsigned)x * m) >> kFdivShift);
 }
 __device__ __forceinline__ unsigned smid() {
   unsigned s;
@@ -496,12 +505,14 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>:
 }
 
 // Stage 2 (twostage.py:175-205): y = +0.0 + p_0 + p_1 + ... + p_{k-1}, every
-// add rounded (FADD, never contracted).  HBM-bound streaming kernel.
+// add rounded (FADD, never contracted).  HBM-bound streaming kernel.  `vec`:
+// total % 4 == 0 and both pointers 16-byte aligned (decided by the launcher;
+// a view at an odd float offset takes the scalar loop).
 __global__ void __launch_bounds__(256) stage2_sum_kernel(const float *__restrict__ partials, float *__restrict__ y,
-                                                         long long total, int taps, int pdl) {
+                                                         long long total, int taps, int pdl, int vec) {
   if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // partials come from the previous grid
   const long long stride = (long long)gridDim.x * blockDim.x;
-  if ((total & 3) == 0) {
+  if (vec) {
     const long long total4 = total >> 2;
     const float4 *p4 = reinterpret_cast<const float4 *>(partials);
     float4 *y4 = reinterpret_cast<float4 *>(y);

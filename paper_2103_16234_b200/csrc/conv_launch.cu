@@ -228,7 +228,7 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
   base.rs = rc + (((g.W - rc) % 4) + 4) % 4;  // == W (mod 4): rows stay 16B-congruent with global rows
   base.rows = max_tile_rows(g, hf_eff, f.bp);
   const long long positions = (long long)base.rs * base.rows + 3;
-  if (positions > (1 << 20)) return false;
+  if (positions > kFdivLimit || (long long)g.Hp + base.rows >= kFdivLimit) return false;
   base.tile_elems = rc * base.rows;
   base.xcs = (int)((positions + 3) & ~3LL);
   // relative offsets inside a tile must fit int32 (goff table)
@@ -280,8 +280,24 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
 
 }  // namespace
 
+// mbarrier watchdog of the tensor-core kernels: B2C_WATCHDOG_MS > 0 makes a
+// stalled wait trap after that long (the test suite sets it so a protocol bug
+// cannot hang the GPU); default 0 = unbounded waits (preemption-safe).
+unsigned long long watchdog_ns() {
+  static const unsigned long long ns = [] {
+    const char *e = std::getenv("B2C_WATCHDOG_MS");
+    const long long ms = e ? std::atoll(e) : 0;
+    return ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
+  }();
+  return ns;
+}
+
 bool pdl_enabled() {
+#ifdef B2C_DEV
   static const bool on = std::getenv("B2C_NO_PDL") == nullptr;
+#else
+  static const bool on = true;
+#endif
   return on;
 }
 
@@ -290,7 +306,11 @@ bool pdl_enabled() {
 // 45.8 us) because cross-CTA DSMEM reads run at ~20 B/clk per SM, so parking a
 // 32-64 KB tile costs more than the L2-resident partial planes.
 bool cluster_reduce_enabled() {
+#ifdef B2C_DEV
   static const bool on = std::getenv("B2C_CLUSTER") != nullptr;
+#else
+  static const bool on = false;
+#endif
   return on;
 }
 
@@ -301,8 +321,16 @@ const char *family_name(int id) {
 
 int num_families() { return kNumFamilies; }
 
+// Every quantity the kernels divide with fdiv (pixel offsets within an image
+// plus one tile, virtual rows within an image plus a tile's band) stays below
+// 2^20, where the magic division is exact (conv_kernel.cuh).
+bool fdiv_range_ok(const Geom &g) {
+  return (long long)g.HoWo + 4096 < kFdivLimit && (long long)g.Hp + 4096 < kFdivLimit;
+}
+
 bool family_matches(int fam_id, const Geom &g, bool stage1) {
   if (fam_id < 0 || fam_id >= kNumFamilies) return false;
+  if (!fdiv_range_ok(g)) return false;
   const Family &f = kFamilies[fam_id];
   if (f.strict != stage1) return false;
   if (f.kind == 1)
@@ -484,15 +512,18 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   p.wf_full = g.WF;
   p.y_tap_stride = y_tap_stride;
   p.strict_tap_major = stage1 ? 1 : 0;
-  auto magic = [](int d) { return (unsigned long long)((1ULL << 32) / (unsigned long long)d) + 1ULL; };
-  p.mRS = magic(tc.rs);
-  p.mHp = magic(g.Hp);
-  p.mHoWo = magic(g.HoWo);
-  p.mWo = magic(g.Wo);
+  p.mRS = fdiv_magic(tc.rs);
+  p.mHp = fdiv_magic(g.Hp);
+  p.mHoWo = fdiv_magic(g.HoWo);
+  p.mWo = fdiv_magic(g.Wo);
   p.pdl = pdl_enabled() ? 1 : 0;
   dim3 grid((unsigned)tc.grid, (unsigned)tc.splits, (unsigned)tc.grid_z);
-  // development tracing: per-CTA SM id and start/end globaltimer to a CSV file
+  // development tracing (-DB2C_DEV builds): per-CTA SM id and start/end globaltimer to a CSV file
+#ifdef B2C_DEV
   const char *trace_file = std::getenv("B2C_TRACE_FILE");
+#else
+  const char *trace_file = nullptr;
+#endif
   const long long nctas = tc.grid * tc.splits * tc.grid_z;
   unsigned long long *trace = nullptr;
   if (trace_file && cudaMalloc(&trace, sizeof(unsigned long long) * 5 * nctas) == cudaSuccess) p.trace = trace;
@@ -583,7 +614,9 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
 cudaError_t launch_stage2(const float *partials, float *y, long long total, int taps, int device,
                           cudaStream_t stream) {
   const int sms = sm_count_of(device);
-  const long long work = (total % 4 == 0) ? total / 4 : total;
+  const int vec = (total % 4 == 0) &&
+                  ((reinterpret_cast<uintptr_t>(partials) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+  const long long work = vec ? total / 4 : total;
   long long blocks = std::min<long long>(cdiv(work, 256), (long long)sms * 8);
   if (blocks < 1) blocks = 1;
   note_launch();
@@ -597,7 +630,7 @@ cudaError_t launch_stage2(const float *partials, float *y, long long total, int 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, stage2_sum_kernel, partials, y, total, taps, pdl);
+  return cudaLaunchKernelEx(&cfg, stage2_sum_kernel, partials, y, total, taps, pdl, vec);
 }
 
 }  // namespace b2c

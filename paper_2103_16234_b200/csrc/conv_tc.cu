@@ -47,10 +47,14 @@ constexpr int kSmemBudget = 225 * 1024;  // dynamic smem per CTA incl. 1 KB alig
 
 // 3xTF32 correction products as bf16 MMAs (halo mode).  Default on; B2C_TC_BF16CORR=0 disables.
 bool bf16corr_enabled() {
+#ifdef B2C_DEV
   static const bool on = [] {
     const char *e = std::getenv("B2C_TC_BF16CORR");
     return !(e && std::atoi(e) == 0);
   }();
+#else
+  static const bool on = true;
+#endif
   return on;
 }
 
@@ -337,8 +341,10 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   // kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major
   p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(pl.nf >> 3) << 17) |
             ((uint32_t)(tc::TILE_P >> 4) << 24);
-  p.spin_limit = 4000000000ull;  // 4 s
+  p.spin_limit = watchdog_ns();
+#ifdef B2C_DEV
   if (const char *m = std::getenv("B2C_TC_MODE")) p.mode = std::atoi(m);
+#endif
 
   const void *kern = tc_kernel(kpasses, pl.halo > 0, pl.mh);
   // once per (kernel, device): allow the full opt-in shared memory, so launches
@@ -371,8 +377,12 @@ cudaError_t launch_tc(const Geom &g, const TcPlan &pl, const float *x, const flo
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  // development dump (B2C_TC_DEBUG=path): timeout code, CTA-0 stage 0 and accumulator
+  // development dump (-DB2C_DEV builds, B2C_TC_DEBUG=path): timeout code, CTA-0 stage 0 and accumulator
+#ifdef B2C_DEV
   const char *dbg_file = std::getenv("B2C_TC_DEBUG");
+#else
+  const char *dbg_file = nullptr;
+#endif
   const size_t dbg_words = 16 + 65536 + 128 * 256;
   unsigned *dbg_host = nullptr;  // mapped pinned memory: readable even after a device trap
   if (dbg_file && cudaHostAlloc(reinterpret_cast<void **>(&dbg_host), dbg_words * 4, cudaHostAllocMapped) == cudaSuccess) {

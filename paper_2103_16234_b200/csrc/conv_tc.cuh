@@ -84,11 +84,21 @@ struct TcParams {
   int stage_bytes;   // (A_BYTES + b_bytes) * (PASSES == 3 ? 2 : 1)
   int tmem_cols;
   uint32_t idesc;    // UMMA instruction descriptor (kind::tf32, M=128, N=NF)
-  unsigned long long spin_limit;  // mbarrier wait bound (ns) before __trap: no silent hangs
-  int mode;                       // development only (B2C_TC_MODE): 1 skip gather, 2 skip MMA, 4 skip B split,
+  unsigned long long spin_limit;  // mbarrier wait bound (ns) before __trap; 0 = unbounded (watchdog_ns())
+  int mode;                       // development builds only (-DB2C_DEV, B2C_TC_MODE): 1 skip gather, 2 skip MMA, 4 skip B split,
                                   // 8 skip filter copy, 16 skip proxy fence, 32 skip A stores, 128 dumps
-  unsigned int *dbg;              // development only (B2C_TC_DEBUG): wait-timeout codes and CTA-0 dumps
+  unsigned int *dbg;              // development builds only (-DB2C_DEV, B2C_TC_DEBUG): wait-timeout codes and CTA-0 dumps
 };
+
+// Development instrumentation (role skipping, CTA-0 cycle dumps) exists only in
+// builds with -DB2C_DEV (tools/ab_lib.sh); release builds compile it out.
+#ifdef B2C_DEV
+#define TC_MODE(bit) (p.mode & (bit))
+#define TC_DBG p.dbg
+#else
+#define TC_MODE(bit) 0
+#define TC_DBG (static_cast<unsigned int *>(nullptr))
+#endif
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -113,14 +123,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
-// `limit_ns` is wall time (globaltimer), checked every 256 polls.
+// mbarrier wait.  limit_ns == 0 (default): unbounded — a correct kernel may be
+// preempted or time-sliced for any length of time.  limit_ns > 0 (watchdog,
+// B2C_WATCHDOG_MS, set by the test suite): a protocol bug traps (kernel error)
+// instead of hanging the GPU; wall time (globaltimer), checked every 256 polls.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, unsigned long long limit_ns,
                                           unsigned int *dbg = nullptr, unsigned code = 0) {
   unsigned long long t0 = 0;
   unsigned n = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 255u) == 0) {
+    if (limit_ns && (++n & 255u) == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t0 == 0) {
@@ -171,26 +183,10 @@ __device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
   asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
 
-__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1, int c2,
-                                            int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
-      "[%2];" ::"r"(dst),
-      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,
-                                            int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
-      "[%2];" ::"r"(dst),
-      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
 }
 
 // UMMA shared-memory descriptor (sm100 layout: start>>4 [0,14), LBO>>4 [16,30),
@@ -323,15 +319,15 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
     const bool leader = elect_one();
     {
       // ------------------------------------------------ filter-tile bulk-copy producer
-      const bool prof = p.dbg && blockIdx.x == 0 && leader;
+      const bool prof = TC_DBG && blockIdx.x == 0 && leader;
       unsigned long long qt_wait = 0;
       const unsigned long long qt_start = prof ? clock64() : 0;
       for (int kb = 0; kb < KB; kb++) {
         const int s = kb % S;
         const unsigned long long c0 = prof ? clock64() : 0;
-        if (kb >= S) mbar_wait(empty_bar(s), ((kb / S) - 1) & 1, p.spin_limit, p.dbg, 0x100000u | kb);
+        if (kb >= S) mbar_wait(empty_bar(s), ((kb / S) - 1) & 1, p.spin_limit, TC_DBG, 0x100000u | kb);
         if (prof) qt_wait += clock64() - c0;
-        if (p.mode & 8) {
+        if (TC_MODE(8)) {
           if (leader) mbar_arrive(full_bar(s));
           continue;
         }
@@ -343,13 +339,13 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
         }
         __syncwarp();
       }
-      if (prof) { p.dbg[5] = (unsigned)qt_wait; p.dbg[6] = (unsigned)(clock64() - qt_start); }
+      if (prof) { TC_DBG[5] = (unsigned)qt_wait; TC_DBG[6] = (unsigned)(clock64() - qt_start); }
     }
   } else if (warp == 1) {
     const bool leader = elect_one();
     {
       // ------------------------------------------------------------ MMA issuer
-      const bool prof = p.dbg && blockIdx.x == 0 && leader;
+      const bool prof = TC_DBG && blockIdx.x == 0 && leader;
       unsigned long long mt_wait = 0, mt_issue = 0;
       const unsigned long long mt_start = prof ? clock64() : 0;
       // both operands: no-swizzle K-major core matrices, LBO 128 B (K), SBO 512 B (rows)
@@ -363,14 +359,14 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
         const int s = kb % S;
         const uint32_t ph = (kb / S) & 1;
         unsigned long long c0 = prof ? clock64() : 0;
-        mbar_wait(full_bar(s), ph, p.spin_limit, p.dbg, 0x200000u | kb);
-        mbar_wait(ready_bar(s), ph, p.spin_limit, p.dbg, 0x280000u | kb);
+        mbar_wait(full_bar(s), ph, p.spin_limit, TC_DBG, 0x200000u | kb);
+        mbar_wait(ready_bar(s), ph, p.spin_limit, TC_DBG, 0x280000u | kb);
         tc_fence_after();
         if (prof) { const unsigned long long c = clock64(); mt_wait += c - c0; c0 = c; }
         // descriptors advanced by adding 16-byte units to the start-address field
         const uint64_t a0 = a_desc0 + (((uint32_t)s * p.stage_bytes) >> 4);
         const uint64_t b0 = a0 + (b_off >> 4);
-        if (leader && !(p.mode & 2)) {
+        if (leader && !TC_MODE(2)) {
 #pragma unroll
           for (int k = 0; k < BC / 8; k++) {
             const uint32_t acc = (kb | k) != 0;
@@ -393,7 +389,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
         if (prof) mt_issue += clock64() - c0;
       }
       if (leader) umma_commit(accum_bar);
-      if (prof) { p.dbg[3] = (unsigned)mt_wait; p.dbg[4] = (unsigned)mt_issue; p.dbg[2] = (unsigned)(clock64() - mt_start); }
+      if (prof) { TC_DBG[3] = (unsigned)mt_wait; TC_DBG[4] = (unsigned)mt_issue; TC_DBG[2] = (unsigned)(clock64() - mt_start); }
     }
   } else {
     const int lt = threadIdx.x - 64;  // 0..LOADERS-1
@@ -455,24 +451,24 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
       const int kx = t - ky * p.WF;
       const int c0 = cb * BC + cgrp * CH_PER_LOADER;
       const int iy = iy0 + ky, ix = ix0 + kx;
-      const bool ok = pbase >= 0 && iy >= 0 && iy < Hh && ix >= 0 && ix < Ww && !(p.mode & 1);
+      const bool ok = pbase >= 0 && iy >= 0 && iy < Hh && ix >= 0 && ix < Ww && !TC_MODE(1);
       const float *src = xg + pbase + (long long)c0 * p.HW + iy * Ww + ix;
       const int nc = ok ? min(CH_PER_LOADER, p.C - c0) : 0;
 #pragma unroll
       for (int j = 0; j < CH_PER_LOADER; j++) v[j] = j < nc ? __ldg(src + (long long)j * p.HW) : 0.0f;
     };
-    const bool prof = p.dbg && blockIdx.x == 0 && lt == 0;  // development timing of loader warp 2
+    const bool prof = TC_DBG && blockIdx.x == 0 && lt == 0;  // development timing of loader warp 2
     unsigned long long pt_wait_e = 0, pt_store = 0, pt_fence = 0, pt_gather = 0;
     auto commit = [&](int kb, const float (&v)[CH_PER_LOADER]) {
       const int s = kb % S;
       unsigned long long c0 = prof ? clock64() : 0;
       if (kb >= S) {  // one lane polls, the warp follows
-        if (lane == 0) mbar_wait(empty_bar(s), ((kb / S) - 1) & 1, p.spin_limit, p.dbg, 0x300000u | kb);
+        if (lane == 0) mbar_wait(empty_bar(s), ((kb / S) - 1) & 1, p.spin_limit, TC_DBG, 0x300000u | kb);
         __syncwarp();
       }
       if (prof) { const unsigned long long c = clock64(); pt_wait_e += c - c0; c0 = c; }
       const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes + a_row;
-      if (!(p.mode & 32)) {
+      if (!TC_MODE(32)) {
         sts128(st, make_float4(v[0], v[1], v[2], v[3]));  // the tensor core reads tf32 = v truncated
         sts128(st + 128, make_float4(v[4], v[5], v[6], v[7]));
         if (PASSES == 3) {
@@ -491,7 +487,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
       if (prof) { const unsigned long long c = clock64(); pt_store += c - c0; c0 = c; }
       // generic-proxy smem writes -> visible to the tensor core (async proxy);
       // one arrival per warp
-      if (!(p.mode & 16)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (!TC_MODE(16)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(ready_bar(s));
       if (prof) pt_fence += clock64() - c0;
@@ -515,11 +511,11 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_kernel(const __grid_consta
       }
     }
     if (prof) {
-      p.dbg[7] = (unsigned)pt_wait_e; p.dbg[8] = (unsigned)pt_store; p.dbg[11] = (unsigned)pt_fence;
-      p.dbg[12] = (unsigned)pt_gather; p.dbg[13] = (unsigned)(clock64() - pt_start);
+      TC_DBG[7] = (unsigned)pt_wait_e; TC_DBG[8] = (unsigned)pt_store; TC_DBG[11] = (unsigned)pt_fence;
+      TC_DBG[12] = (unsigned)pt_gather; TC_DBG[13] = (unsigned)(clock64() - pt_start);
     }
     // ------------------------------------------------------------------ epilogue
-    if (lane == 0) mbar_wait(accum_bar, 0, p.spin_limit, p.dbg, 0x400000u);
+    if (lane == 0) mbar_wait(accum_bar, 0, p.spin_limit, TC_DBG, 0x400000u);
     __syncwarp();
     tc_fence_after();
     const int q = warp & 3;              // TMEM lane quarter this warp may access
@@ -641,7 +637,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_d = *tmem_slot;
-  if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 64) p.dbg[11] = (unsigned)clock64();
+  if (TC_DBG && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 64) TC_DBG[11] = (unsigned)clock64();
   // TMEM columns: main accumulator of half h at h*NF, 3xTF32 correction at (MH+h)*NF
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
@@ -649,18 +645,18 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
     const bool leader = elect_one();
     {
       // ------------------------------------------- filter-tile (hi plane) bulk copies
-      const bool prof = p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && leader;
+      const bool prof = TC_DBG && blockIdx.x == 0 && blockIdx.y == 0 && leader;
       unsigned long long qt_wait = 0;
       const unsigned long long qt_start = prof ? clock64() : 0;
       for (int kb = 0; kb < KB; kb++) {
         const int s = kb % S;
         const unsigned long long c0 = prof ? clock64() : 0;
-        if (kb >= S) mbar_wait(b_empty(s), ((kb / S) - 1) & 1, p.spin_limit, p.dbg, 0x110000u | kb);
+        if (kb >= S) mbar_wait(b_empty(s), ((kb / S) - 1) & 1, p.spin_limit, TC_DBG, 0x110000u | kb);
         if (prof) qt_wait += clock64() - c0;
         const uint32_t bytes = b_stage;  // fp32 hi [+ lo, or bf16 hi + lo] planes, one contiguous block
         const float *src = p.wt + ((long long)(cb_base * p.taps + kb) * p.mtiles + mt) * (bytes / 4);
         if (leader) {
-          if (p.mode & 8) {
+          if (TC_MODE(8)) {
             mbar_arrive(b_full(s));
           } else {
             mbar_expect_tx(b_full(s), bytes);
@@ -669,7 +665,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
         }
         __syncwarp();
       }
-      if (prof) { p.dbg[5] = (unsigned)qt_wait; p.dbg[6] = (unsigned)(clock64() - qt_start); }
+      if (prof) { TC_DBG[5] = (unsigned)qt_wait; TC_DBG[6] = (unsigned)(clock64() - qt_start); }
     }
   } else if (warp == 1) {
     const bool leader = elect_one();
@@ -678,7 +674,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
       // Descriptors are built once per buffer / stage and advanced by adding
       // the 16-byte-unit offset to their start-address field (all operand
       // addresses stay below 256 KB, so the 14-bit field never carries).
-      const bool prof = p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && leader;
+      const bool prof = TC_DBG && blockIdx.x == 0 && blockIdx.y == 0 && leader;
       unsigned long long mt_wait = 0, mt_wait_a = 0;
       const unsigned long long mt_start = prof ? clock64() : 0;
       const uint64_t a_desc0 = umma_desc(smem_base, a_plane, 128, LAYOUT_NONE);
@@ -695,7 +691,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
       for (int i = 0; i < NCB; i++) {
         const int buf = i % SA;
         unsigned long long c0 = prof ? clock64() : 0;
-        mbar_wait(a_full(buf), (i / SA) & 1, p.spin_limit, p.dbg, 0x210000u | i);
+        mbar_wait(a_full(buf), (i / SA) & 1, p.spin_limit, TC_DBG, 0x210000u | i);
         if (prof) mt_wait_a += clock64() - c0;
         tc_fence_after();
         const uint64_t a_buf_desc = a_desc0 + ((buf * a_buf) >> 4);
@@ -704,7 +700,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
           const int kb = i * taps + t;
           const int s = kb % S;
           c0 = prof ? clock64() : 0;
-          mbar_wait(b_full(s), (kb / S) & 1, p.spin_limit, p.dbg, 0x220000u | kb);
+          mbar_wait(b_full(s), (kb / S) & 1, p.spin_limit, TC_DBG, 0x220000u | kb);
           if (prof) mt_wait += clock64() - c0;
           tc_fence_after();
           const uint64_t a0 = a_buf_desc + (uint64_t)((ky * wp + kx) & 0xFFFF);  // tap shift: 16 B per position
@@ -720,7 +716,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
               // half, then the correction terms) so their latencies overlap
 #pragma unroll
               for (int h = 0; h < MH; h++)
-                if (!(p.mode & 2)) umma_tf32(tmem_d + h * nf, ak + h * (TILE_P * 16 >> 4), bh, idesc, acc);
+                if (!TC_MODE(2)) umma_tf32(tmem_d + h * nf, ak + h * (TILE_P * 16 >> 4), bh, idesc, acc);
               if (PASSES == 2 && k == 0) {
                 // bf16 corrections over the whole 16-channel block (one K=16 MMA each)
                 const uint32_t acc16 = kb != 0;
@@ -728,23 +724,23 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
 #pragma unroll
                 for (int h = 0; h < MH; h++) {
                   const uint64_t ah16 = a0 + (a_bytes >> 4) + h * (TILE_P * 16 >> 4);
-                  if (!(p.mode & 2)) {
+                  if (!TC_MODE(2)) {
                     umma_f16(tmem_d + (MH + h) * nf, ah16, bl16, idesc16, acc16);
                   }
                 }
 #pragma unroll
                 for (int h = 0; h < MH; h++) {
                   const uint64_t al16 = a0 + ((a_bytes + a_bytes / 2) >> 4) + h * (TILE_P * 16 >> 4);
-                  if (!(p.mode & 2)) umma_f16(tmem_d + (MH + h) * nf, al16, bh16, idesc16, 1);
+                  if (!TC_MODE(2)) umma_f16(tmem_d + (MH + h) * nf, al16, bh16, idesc16, 1);
                 }
               }
               if (PASSES == 3) {
 #pragma unroll
                 for (int h = 0; h < MH; h++)
-                  if (!(p.mode & 2)) umma_tf32(tmem_d + (MH + h) * nf, ak + h * (TILE_P * 16 >> 4), bl, idesc, acc);
+                  if (!TC_MODE(2)) umma_tf32(tmem_d + (MH + h) * nf, ak + h * (TILE_P * 16 >> 4), bl, idesc, acc);
 #pragma unroll
                 for (int h = 0; h < MH; h++)
-                  if (!(p.mode & 2))
+                  if (!TC_MODE(2))
                     umma_tf32(tmem_d + (MH + h) * nf, ak + h * (TILE_P * 16 >> 4) + (a_bytes >> 4), bh, idesc, 1);
               }
             }
@@ -760,7 +756,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
         __syncwarp();
       }
       if (leader) umma_commit(accum_bar);
-      if (prof) { p.dbg[3] = (unsigned)mt_wait; p.dbg[4] = (unsigned)mt_wait_a; p.dbg[2] = (unsigned)(clock64() - mt_start); }
+      if (prof) { TC_DBG[3] = (unsigned)mt_wait; TC_DBG[4] = (unsigned)mt_wait_a; TC_DBG[2] = (unsigned)(clock64() - mt_start); }
     }
   } else {
     // --------------------------------------- halo loaders (+ filter lo planes)
@@ -770,14 +766,14 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
     const int lt = threadIdx.x - 64;
     const int items = p.halo * 4;
     const float *xg = p.x;
-    const bool prof = p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lt == 0;
+    const bool prof = TC_DBG && blockIdx.x == 0 && blockIdx.y == 0 && lt == 0;
     unsigned long long lt_wait = 0, lt_fill = 0;
     const unsigned long long lt_start = prof ? clock64() : 0;
     for (int i = 0; i < NCB; i++) {
       const int buf = i % SA;
       unsigned long long c0 = prof ? clock64() : 0;
       if (i >= SA) {
-        if (lane == 0) mbar_wait(a_empty(buf), ((i / SA) - 1) & 1, p.spin_limit, p.dbg, 0x310000u | i);
+        if (lane == 0) mbar_wait(a_empty(buf), ((i / SA) - 1) & 1, p.spin_limit, TC_DBG, 0x310000u | i);
         __syncwarp();
       }
       if (prof) { const unsigned long long c = clock64(); lt_wait += c - c0; c0 = c; }
@@ -793,7 +789,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
         const int yy = (int)(r - (long long)n * p.Hp) - p.PH;
         const int c0 = cbase + j * 4;
         float v[4];
-        const bool ok = n < p.N && yy >= 0 && yy < p.H && xx >= 0 && xx < p.W && !(p.mode & 1);
+        const bool ok = n < p.N && yy >= 0 && yy < p.H && xx >= 0 && xx < p.W && !TC_MODE(1);
         const float *src = xg + ((long long)n * p.C + c0) * p.HW + (long long)yy * p.W + xx;
         const int nc = ok ? min(4, p.C - c0) : 0;
 #pragma unroll
@@ -813,13 +809,13 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
       if (lane == 0) mbar_arrive(a_full(buf));
       if (prof) lt_fill += clock64() - c0;
     }
-    if (prof) { p.dbg[7] = (unsigned)lt_wait; p.dbg[8] = (unsigned)lt_fill; p.dbg[13] = (unsigned)(clock64() - lt_start); }
+    if (prof) { TC_DBG[7] = (unsigned)lt_wait; TC_DBG[8] = (unsigned)lt_fill; TC_DBG[13] = (unsigned)(clock64() - lt_start); }
     // ------------------------------------------------------------------ epilogue
     const unsigned long long e0 = prof ? clock64() : 0;
-    if (lane == 0) mbar_wait(accum_bar, 0, p.spin_limit, p.dbg, 0x410000u);
+    if (lane == 0) mbar_wait(accum_bar, 0, p.spin_limit, TC_DBG, 0x410000u);
     __syncwarp();
     tc_fence_after();
-    if (prof) p.dbg[9] = (unsigned)(clock64() - e0);
+    if (prof) TC_DBG[9] = (unsigned)(clock64() - e0);
     const int q = warp & 3;
     const int colgrp = (warp - 2) >> 2;
     constexpr int COLGRPS = LOADERS / 128;
@@ -851,7 +847,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_tc_halo_kernel(const __grid_c
       }
     }
   }
-  if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 64) p.dbg[10] = (unsigned)clock64();
+  if (TC_DBG && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 64) TC_DBG[10] = (unsigned)clock64();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

@@ -70,6 +70,7 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
 cudaError_t launch_stage2(const float *partials, float *y, long long total, int taps, int device,
                           cudaStream_t stream);
 bool pdl_enabled();
+unsigned long long watchdog_ns();
 void register_tuned(const Geom &g, bool stage1, int family, int splits, int reduce = 0);
 void note_launch();
 

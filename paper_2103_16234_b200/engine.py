@@ -7,8 +7,11 @@ caller's current stream (so it composes with CUDA graphs and multi-stream
 code).  PyTorch provides only device memory and the stream: there is no torch
 compute and no fallback — if the native library is absent this raises.
 
-``ConvLayer`` pre-resolves the descriptor and tile plan once for repeated
-calls on one shape (the per-call overhead is then one ctypes call).
+``conv2d`` dispatches through the registered PyTorch operator
+``torch.ops.b2conv.conv2d`` (csrc/torch_ext.cpp, with a Meta kernel for
+fake-tensor tracing); ``ConvLayer`` pre-resolves the descriptor and tile plan
+once for repeated calls on one shape (the per-call overhead is then one ctypes
+call) and is what the benchmark and the sharded wrapper use.
 """
 
 from __future__ import annotations
@@ -88,9 +91,8 @@ class ConvLayer:
             self.workspace_bytes = int(self._tc.workspace_bytes)
         if engine == "twostage" and not (cfg.hf == 1 and cfg.wf == 1):
             self.workspace_bytes = int(self._lib.b2c_workspace_bytes(ctypes.byref(self._desc)))
-        self._ws = None
         self.split_workspace_bytes = int(self._tiles.workspace_bytes) if engine == "fused" else 0
-        self._split_ws = None
+        self._ws_by_stream: dict = {}
 
     @property
     def family(self) -> str:
@@ -119,33 +121,61 @@ class ConvLayer:
     def output_shape(self) -> tuple[int, int, int, int]:
         return (self.cfg.n, self.cfg.m, *self.out_hw)
 
+    def _check_operands(self, x, w, out) -> None:
+        """The operands must match the resolved configuration exactly: the
+        kernels index raw device pointers by ``cfg``, so a mismatch is a
+        ShapeMismatch here, never an out-of-bounds access on the device."""
+        _check_tensor(x, "input")
+        _check_tensor(w, "filters")
+        c = self.cfg
+        if tuple(x.shape) != (c.n, c.c, c.h, c.w):
+            raise ShapeMismatch(f"input has shape {tuple(x.shape)}, layer expects {(c.n, c.c, c.h, c.w)}")
+        if tuple(w.shape) != (c.m, c.c, c.hf, c.wf):
+            raise ShapeMismatch(f"filters have shape {tuple(w.shape)}, layer expects {(c.m, c.c, c.hf, c.wf)}")
+        if w.device != x.device:
+            raise ShapeMismatch("input and filters must be on the same device")
+        if out is not None:
+            _check_tensor(out, "out")
+            if tuple(out.shape) != self.output_shape():
+                raise ShapeMismatch(f"out has shape {tuple(out.shape)}, expected {self.output_shape()}")
+            if out.device != x.device:
+                raise ShapeMismatch("out must be on the input's device")
+
+    def _workspace(self, nbytes: int, device, stream_handle: int):
+        """Scratch (split-C partial planes, pre-tiled filters) private to one
+        (device, stream): calls on different streams never share it, calls on
+        one stream are ordered by the stream."""
+        import torch
+
+        key = (device.index, stream_handle)
+        buf = self._ws_by_stream.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = self._ws_by_stream[key] = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        return buf.data_ptr()
+
     def __call__(self, x, w, out=None, stream=None):
         import torch
 
+        self._check_operands(x, w, out)
         if out is None:
             out = torch.empty(self.output_shape(), dtype=torch.float32, device=x.device)
         s = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
         if self.engine == "fused":
             ws_ptr, ws_len = None, 0
             if self.split_workspace_bytes:
-                if self._split_ws is None or self._split_ws.device != x.device:
-                    self._split_ws = torch.empty(self.split_workspace_bytes, dtype=torch.uint8, device=x.device)
-                ws_ptr, ws_len = self._split_ws.data_ptr(), self.split_workspace_bytes
+                ws_len = self.split_workspace_bytes
+                ws_ptr = self._workspace(ws_len, x.device, s)
             st = self._lib.b2c_conv2d_forward(ctypes.byref(self._desc), x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                               ws_ptr, ws_len, ctypes.byref(self._tiles), ctypes.c_void_p(s))
             nat.check(st)
         elif self.tensor_core:
-            if self.workspace_bytes and (self._ws is None or self._ws.device != x.device):
-                self._ws = torch.empty(self.workspace_bytes // 4, dtype=torch.float32, device=x.device)
-            ws_ptr = self._ws.data_ptr() if self.workspace_bytes else None
+            ws_ptr = self._workspace(self.workspace_bytes, x.device, s) if self.workspace_bytes else None
             st = self._lib.b2c_conv2d_forward_tc(ctypes.byref(self._desc), x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                                  ws_ptr, self.workspace_bytes, self._engine_id, ctypes.byref(self._tc),
                                                  ctypes.c_void_p(s))
             nat.check(st)
         else:
-            if self.workspace_bytes and (self._ws is None or self._ws.device != x.device):
-                self._ws = torch.empty(self.workspace_bytes // 4, dtype=torch.float32, device=x.device)
-            ws_ptr = self._ws.data_ptr() if self.workspace_bytes else None
+            ws_ptr = self._workspace(self.workspace_bytes, x.device, s) if self.workspace_bytes else None
             stats = nat.RunStatsC()
             st = self._lib.b2c_conv_twostage(ctypes.byref(self._desc), x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                              ws_ptr, self.workspace_bytes, None, None, 1 << 62, ctypes.c_void_p(s),
@@ -154,22 +184,48 @@ class ConvLayer:
         return out
 
 
-_layer_cache: dict = {}
+_ops_loaded = False
+
+
+def torch_ops():
+    """``torch.ops.b2conv`` — the PyTorch operator library (csrc/torch_ext.cpp,
+    built in-tree as _b2conv_torch.so next to libb2conv.so).  Raises
+    DeviceError if it is missing: there is no fallback."""
+    global _ops_loaded
+    import torch
+
+    if not _ops_loaded:
+        from .build import TORCH_LIB
+
+        nat.lib()  # libb2conv.so first: the operator library links it
+        if not TORCH_LIB.exists():
+            raise nat.DeviceError(f"{TORCH_LIB.name} is not built (python -m paper_2103_16234_b200.build)")
+        torch.ops.load_library(str(TORCH_LIB))
+        _ops_loaded = True
+    return torch.ops.b2conv
 
 
 def conv2d(x, w, stride=1, padding=0, *, engine: str = "fused", out=None):
-    """``F.conv2d(x, w, stride=stride, padding=padding)`` on B200 kernels."""
+    """``F.conv2d(x, w, stride=stride, padding=padding)`` on B200 kernels,
+    through the registered operator ``torch.ops.b2conv.conv2d`` (traceable by
+    torch.compile / torch.export through its Meta kernel).  Operand errors
+    raise the reference's exception classes first (ShapeMismatch,
+    Unsupported, InvalidConfig)."""
+    if engine not in nat.ENGINES:
+        raise ValueError(f"unknown engine {engine!r}")
     _check_tensor(x, "input")
     _check_tensor(w, "filters")
     if w.device != x.device:
         raise ShapeMismatch("input and filters must be on the same device")
     cfg = config_for(x, w, stride, padding)
-    key = (cfg.as_tuple(), engine, x.device.index)
-    layer = _layer_cache.get(key)
-    if layer is None:
-        layer = _layer_cache[key] = ConvLayer(cfg, engine)
-    if out is not None:
-        _check_tensor(out, "out")
-        if tuple(out.shape) != layer.output_shape():
-            raise ShapeMismatch(f"out has shape {tuple(out.shape)}, expected {layer.output_shape()}")
-    return layer(x, w, out=out)
+    if engine == "twostage" and cfg.stride != 1:
+        raise Unsupported(f"two-stage convolution requires stride 1, got {cfg.stride}")
+    st, pd = [cfg.stride, cfg.stride], [cfg.pad_h, cfg.pad_w]
+    ops = torch_ops()
+    if out is None:
+        return ops.conv2d(x, w, st, pd, engine)
+    _check_tensor(out, "out")
+    want = (cfg.n, cfg.m, *output_dims(cfg))
+    if tuple(out.shape) != want:
+        raise ShapeMismatch(f"out has shape {tuple(out.shape)}, expected {want}")
+    return ops.conv2d_out(x, w, st, pd, engine, out=out)
