@@ -22,9 +22,15 @@
  *    reference's exception classes (errors.py:9-61) in the reference's
  *    precedence: Unsupported(stride) -> ShapeMismatch -> InvalidPlan ->
  *    WorkspaceExceeded (twostage.py:73-79, 214-224).
- *  - Results are bitwise independent of the tile plan and of how a batch is
- *    sharded across GPUs (each output's summation order depends only on
- *    c, hf, wf), mirroring SPEC.md:315,326.
+ *  - Determinism: every engine is deterministic run to run
+ *    (no atomics on data).  Each output's summation order is a function of
+ *    (c, hf, wf) for the paper-faithful two-stage engine — bitwise
+ *    independent of any plan — of (c, hf, wf, splits) for the fused engine
+ *    (independent of the kernel family and of the split-C reduction mode),
+ *    and of (mode, splits) for the tensor-core engines.  Images are
+ *    independent, so a batch sharded across GPUs is bitwise identical to the
+ *    unsharded result when each shard runs the global plan's splits
+ *    (sharding.shard_layer pins them).
  */
 #ifndef B2CONV_H
 #define B2CONV_H
@@ -273,8 +279,9 @@ b2c_status b2c_stage2_host(const b2c_conv_desc *d, const float *partials_host, f
                            int32_t device, b2c_run_stats *stats);
 
 /* FP32 roofline denominator: times an FFMA2 (fma.rn.f32x2) register-blocked
- * loop on every SM; returns TFLOP/s (CUDA events), FMA/clk/SM and the SM clock
- * achieved during the probe (in-kernel clock64). */
+ * loop on every SM; returns TFLOP/s (CUDA events), the SM clock the probe ran
+ * at (per-CTA clock64 cycles / globaltimer ns) and FMA/clk/SM = FMAs / (SMs x
+ * wall time x clock), whose hardware ceiling is 128 (FP32 lanes per SM). */
 b2c_status b2c_probe_fp32_peak(int32_t iters, double *tflops, double *fma_per_clk_per_sm, double *sm_mhz);
 
 /* Pinned host memory helpers (so e2e callers can stage through page-locked

@@ -143,7 +143,11 @@ struct Candidate {
 // partial traffic.  (Coefficients fitted on B200 timings of the BASELINE
 // layers.)
 double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, int sms, int max_blocks) {
-  const double fma = (double)tc.bm * tc.bp * taps * tc.bc * tc.chunks_per_split * (stage1 ? 2.0 : 1.0);
+  // the halo-staged kernel on a 1x1 filter issues 4 LDS.128 + 4 LDS.32 per 32
+  // FFMA2 against the pointwise kernels' 4 LDS.128 (measured: the pointwise
+  // families win every 1x1 layer with H*W % 4 == 0 they can run, tuned_plans.json)
+  const double lds_penalty = (!stage1 && tc.kind == 0 && taps == 1) ? 1.25 : 1.0;
+  const double fma = (double)tc.bm * tc.bp * taps * tc.bc * tc.chunks_per_split * (stage1 ? 2.0 : 1.0) * lds_penalty;
   const double per_elem = (tc.kind == 1 || ((long long)g.H * g.W % 4 == 0 && tc.kind == 0)) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
   const double loads = (per_elem * tc.tile_elems + 4.0 * tc.bm * taps) * tc.bc * tc.chunks_per_split;
   const double fixed = 250000.0 + 12.0 * tc.tile_elems;

@@ -7,10 +7,14 @@ collective on the hot path.  Only when a single-device result is requested is
 the NCHW output gathered (NCCL over NVLink on GPUs; any torch.distributed
 backend works, gloo is used by the CPU tests).
 
-Per image, the arithmetic does not depend on the shard: the two-stage engine
-is bitwise identical for any world size, and the fused engine is too when the
-reduction split is pinned (``splits=``), since its planner otherwise adapts
-the split to the per-rank batch.
+Per image, the arithmetic does not depend on the shard (the
+reference's worker independence, test_acceptance.py:179-213):
+the two-stage engine's order is fixed by (c, hf, wf); the fused engine's by
+(c, hf, wf, splits) and the tensor-core engines' by (mode, splits).  The
+planner would adapt the split to the per-rank batch, so ``shard_layer`` pins
+every order-relevant plan field to the plan of the GLOBAL batch: a rank's slab
+is then bitwise identical to the same images of the unsharded result for any
+world size (tests/test_gpu_sharding.py).
 """
 
 from __future__ import annotations
@@ -32,6 +36,38 @@ def shard_config(cfg: ConvConfig, world: int, rank: int) -> ConvConfig:
     return cfg.with_batch(max(hi - lo, 0)) if hi > lo else cfg.with_batch(1)
 
 
+def shard_layer(cfg: ConvConfig, local_cfg: ConvConfig, engine: str = "fused"):
+    """The ConvLayer a rank runs for its slab ``local_cfg`` of the global
+    layer ``cfg``, with the summation-order fields of its plan pinned to the
+    global plan (fused: split-C count; tensor core: A-operand mode and
+    split-K count), so its outputs do not depend on the world size.  The
+    slab's own plan (measured registry or planner) is kept whenever it already
+    agrees; otherwise its kernel family / filters-per-tile are kept and only
+    the order-relevant fields are forced."""
+    from .engine import ConvLayer
+    from .errors import InvalidPlan
+
+    local = ConvLayer(local_cfg, engine)
+    if local_cfg.as_tuple() == cfg.as_tuple() or engine == "twostage":
+        return local
+    ref = ConvLayer(cfg, engine)
+    if engine == "fused":
+        if local.splits == ref.splits:
+            return local
+        reduce = ref.reduce if ref.splits > 1 else 0
+        try:
+            return ConvLayer(local_cfg, engine, family=int(local._tiles.family), splits=ref.splits, reduce=reduce)
+        except InvalidPlan:
+            return ConvLayer(local_cfg, engine, splits=ref.splits, reduce=reduce)
+    if local.splits == ref.splits and int(local._tc.mode) == int(ref._tc.mode):
+        return local
+    try:
+        return ConvLayer(local_cfg, engine, splits=ref.splits, tc_mode=int(ref._tc.mode),
+                         filters_per_tile=int(local._tc.filters_per_tile))
+    except InvalidPlan:
+        return ConvLayer(local_cfg, engine, splits=ref.splits, tc_mode=int(ref._tc.mode))
+
+
 class ShardedConv:
     """Forward convolution of a global batch split across ``world`` ranks.
 
@@ -40,8 +76,7 @@ class ShardedConv:
     callable to exercise the sharding/gather plumbing on CPU.
     """
 
-    def __init__(self, cfg: ConvConfig, group=None, engine: str = "fused", splits: int = 0,
-                 compute: Optional[Callable] = None):
+    def __init__(self, cfg: ConvConfig, group=None, engine: str = "fused", compute: Optional[Callable] = None):
         import torch.distributed as dist
 
         self.cfg = cfg
@@ -52,9 +87,7 @@ class ShardedConv:
         self.local_cfg = cfg.with_batch(self.hi - self.lo) if self.hi > self.lo else None
         self._compute = compute
         if compute is None and self.local_cfg is not None:
-            from .engine import ConvLayer
-
-            self._layer = ConvLayer(self.local_cfg, engine, splits=splits)
+            self._layer = shard_layer(cfg, self.local_cfg, engine)
             self._compute = lambda c, x, w: self._layer(x, w)
 
     def local_slice(self, x_global):
@@ -66,7 +99,12 @@ class ShardedConv:
         import torch.distributed as dist
 
         if self.world > 1:
-            dist.broadcast(w, src, group=self.group)
+            if w.is_cuda and dist.get_backend(self.group) == "gloo":
+                h = w.cpu()
+                dist.broadcast(h, src, group=self.group)
+                w.copy_(h)
+            else:
+                dist.broadcast(w, src, group=self.group)
         return w
 
     def forward(self, x_local, w):
@@ -77,8 +115,10 @@ class ShardedConv:
 
     def gather(self, y_local, dst: Optional[int] = None):
         """Assemble the global [n, m, ho, wo] output on every rank
-        (``dst=None``) or on rank ``dst`` only (others get None).  Slabs are
-        padded to the largest shard so one all_gather suffices."""
+        (``dst=None``: one all_gather) or on rank ``dst`` only (one gather:
+        the other ranks send their slab and get None).  Slabs are padded to
+        the largest shard so every rank moves the same byte count; NCCL over
+        NVLink on GPUs, gloo on CPU."""
         import torch
         import torch.distributed as dist
 
@@ -89,16 +129,26 @@ class ShardedConv:
 
         ho, wo = output_dims(self.cfg)
         dev = y_local.device if y_local is not None else torch.device("cpu")
-        pad = torch.zeros((biggest, self.cfg.m, ho, wo), dtype=torch.float32, device=dev)
-        if y_local is not None:
-            pad[: y_local.shape[0]].copy_(y_local)
-        parts = [torch.empty_like(pad) for _ in range(self.world)]
-        dist.all_gather(parts, pad, group=self.group)
-        if dst is not None and self.rank != dst:
-            return None
-        out = [p[: shard_range(self.cfg.n, self.world, r)[1] - shard_range(self.cfg.n, self.world, r)[0]]
-               for r, p in enumerate(parts)]
-        return torch.cat(out, dim=0)
+        if y_local is not None and y_local.shape[0] == biggest and y_local.is_contiguous():
+            pad = y_local
+        else:
+            pad = torch.zeros((biggest, self.cfg.m, ho, wo), dtype=torch.float32, device=dev)
+            if y_local is not None:
+                pad[: y_local.shape[0]].copy_(y_local)
+        on_host = pad.is_cuda and dist.get_backend(self.group) == "gloo"
+        if on_host:  # gloo moves host memory; NCCL (the GPU backend) gathers device memory directly
+            pad = pad.cpu()
+        if dst is None:
+            parts = [torch.empty_like(pad) for _ in range(self.world)]
+            dist.all_gather(parts, pad, group=self.group)
+        else:
+            parts = [torch.empty_like(pad) for _ in range(self.world)] if self.rank == dst else None
+            dist.gather(pad, parts, dst=dst, group=self.group)
+            if self.rank != dst:
+                return None
+        sizes = [shard_range(self.cfg.n, self.world, r) for r in range(self.world)]
+        out = torch.cat([p[: hi - lo] for (lo, hi), p in zip(sizes, parts)], dim=0)
+        return out.to(dev) if on_host else out
 
     def __call__(self, x_local, w, gather: bool = False, dst: Optional[int] = None):
         y = self.forward(x_local, w)

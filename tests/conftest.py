@@ -12,6 +12,9 @@ import numpy as np
 import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
+# tensor-core mbarrier watchdog for the suite: a protocol bug traps after 20 s
+# instead of hanging the GPU (release default: unbounded waits)
+os.environ.setdefault("B2C_WATCHDOG_MS", "20000")
 sys.path.insert(0, str(ROOT))
 GOLDEN = Path(__file__).resolve().parent / "golden"
 

@@ -459,11 +459,20 @@ def test_bench_dominant_kernel_roofline_fields(tmp_path, monkeypatch):
     path.write_text(json.dumps({"c2": {cfgs[i].name: {"family": layers[i].family, "dram_bytes": 1000 + i}
                                        for i in idx}}))
     monkeypatch.setattr(bench, "TRAFFIC_PATH", str(path))
-    d = bench.dominant_kernel(cfgs, layers, ms, "c2")
+    d = bench.dominant_kernel(cfgs, layers, ms, "c2", 72.0, 6500.0)
     assert d["kernel"] == fam and d["launches"] == len(idx)
+    ridge = 72.0e12 / 6500.0e9
+    fl, by = sum(cfgs[i].flops for i in idx), sum(cfgs[i].compulsory_bytes for i in idx)
+    assert d["bound"] == ("fp32" if fl / by >= ridge else "hbm")
+    assert abs(d["share"] - sum(ms[i] for i in idx) / sum(ms)) < 1e-4
     assert abs(d["achieved_tflops"] - sum(cfgs[i].flops for i in idx) / (sum(ms[i] for i in idx) * 1e-3) / 1e12) < 1e-9
     assert d["traffic"] == round(sum(1000 + i for i in idx) / len(idx)) and d["traffic_source"]
-    assert bench.dominant_kernel(cfgs, layers, ms, "c3")["traffic"] is None  # no capture for that workload
+    assert bench.dominant_kernel(cfgs, layers, ms, "c3", 72.0, 6500.0)["traffic"] is None  # no capture for it
+    rows = bench.layer_rooflines(cfgs, layers, ms, 72.0, 6500.0)
+    assert [r["layer"] for r in rows] == [c.name for c in cfgs]
+    for r, c, t in zip(rows, cfgs, ms):
+        want = (c.flops / (t * 1e-3) / 72.0e12) if r["bound"] == "fp32" else c.compulsory_bytes / (t * 1e-3) / 6500.0e9
+        assert abs(r["roofline_frac"] - want) < 1e-4
 
 
 def test_bench_reference_arm_contract_line():

@@ -1,0 +1,25 @@
+#!/bin/bash
+# ncu evidence for the bench's workload: launch list of the bench command,
+# per-layer DRAM traffic (tools/traffic.py), and `--set full` captures (with
+# source and stall reasons) of the given layers.  Outputs -> gpurun_out/$TAG/.
+#   TAG WORKLOAD N "layer1 layer2 ..."
+TAG=${1:-prof}; WL=${2:-c5}; N=${3:-256}; LAYERS=${4:-}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+export PYTHONUNBUFFERED=1
+python -c "import paper_2103_16234_b200.build as b; b.build()" > "$OUT/build.log" 2>&1
+NCU=/usr/local/cuda/bin/ncu
+if [ -z "$SKIP_LAUNCHES" ]; then
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
+  python bench.py --workload $WL --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline --tc-engine none --layer-passes 1 \
+  > "$OUT/ncu_bench.log" 2>&1
+fi
+if [ -z "$SKIP_TRAFFIC" ]; then
+timeout 900 $NCU --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+  -k regex:"conv|stage2" --csv --log-file "$OUT/traffic_ncu.csv" python tools/traffic.py run $WL > "$OUT/traffic_layers.json" 2> "$OUT/traffic.err"
+fi
+for L in $LAYERS; do
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:conv -s 3 -c 1 \
+    -o "$OUT/full_${WL}_${L}" python tools/prof_layer.py $WL $N $L > "$OUT/full_${WL}_${L}.log" 2>&1
+done
+echo done > "$OUT/DONE"
