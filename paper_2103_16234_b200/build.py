@@ -74,6 +74,35 @@ def build_torch_ext() -> Path:
     return TORCH_LIB
 
 
+def build_dev_variant() -> Path:
+    """libb2conv_dev.so: the same sources with -DB2C_DEV (development switches
+    and instrumentation), loaded by _native when B2C_LIB_VARIANT=dev — for
+    A/B runs on the GPU box only; never the product library."""
+    objdir = PKG / "build_dev"
+    objdir.mkdir(exist_ok=True)
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):
+        obj = objdir / (src.stem + ".o")
+        return obj, subprocess.run([nvcc(), *ARCH, *NVFLAGS, "-DB2C_DEV", "-c", str(src), "-o", str(obj)],
+                                   capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for obj, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stderr)
+            raise RuntimeError("nvcc failed (dev variant)")
+    out = PKG / "libb2conv_dev.so"
+    r = subprocess.run([nvcc(), *ARCH, "-shared", "-Xlinker", "-soname=libb2conv_dev.so", "-o", str(out),
+                        *[str(o) for o, _ in results], "-lcudart_static", "-lpthread", "-ldl", "-lrt"],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stderr)
+        raise RuntimeError("link of libb2conv_dev.so failed")
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not stale():
         return LIB
@@ -111,5 +140,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--dev" in sys.argv:
+        print(build_dev_variant())
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

@@ -59,7 +59,9 @@ struct KParams {
   int ROWS;          // staged virtual rows per channel
   int XCS;           // shared-memory channel stride (floats), multiple of 4, >= ROWS*RS + 3
   int vec_ok;        // H*W % 4 == 0 and x 16B-aligned: 16-byte cp.async groups allowed
+  int vec_out;       // pointwise kernels: Ho*Wo % 4 == 0 and y (and partials) 16B-aligned: float4 stores
   int mtiles;        // ceil(M/BM)
+  int ptiles;        // ceil(Q/BP) (pointwise kernels: work items = mtiles * ptiles * splits)
   int nchunks;       // ceil(C/BC)
   int splits;        // channel ranges reduced separately (blockIdx.y)
   int chunks_per_split;

@@ -37,6 +37,7 @@ struct Family {
   int max_ctas_per_sm;  // from __launch_bounds__
   int kind;             // 0: conv_direct_kernel (halo staging), 1: conv1x1_vec_kernel, 2: its 4-byte variant
   int stages;           // cp.async pipeline depth of kind 1
+  int tm = 2;           // pointwise kernels: channel groups of 4 per thread (4: 16 channels x 8 pixels)
 };
 
 #define B2C_FAMILY(NAME, HF, WF, S, BM, BP, BC, STRICT)                                                    \
@@ -51,6 +52,14 @@ struct Family {
     NAME, 1, 1, 1, Vec1x1Tile<WM, WP, BC>::BM, Vec1x1Tile<WM, WP, BC>::BP, BC, false,                      \
         Vec1x1Tile<WM, WP, BC>::NT, reinterpret_cast<const void *>(&conv1x1_vec_kernel<WM, WP, BC, true>), \
         Vec1x1Tile<WM, WP, BC>::MIN_BLOCKS, 1, Vec1x1Tile<WM, WP, BC>::STAGES                              \
+  }
+// 16 channels x 8 pixels per thread (TM = 4): 128 accumulators, 4-warp CTAs
+#define B2C_VEC1X1W(NAME, WM, WP, BC)                                                                      \
+  Family {                                                                                                 \
+    NAME, 1, 1, 1, Vec1x1Tile<WM, WP, BC, 4>::BM, Vec1x1Tile<WM, WP, BC, 4>::BP, BC, false,                \
+        Vec1x1Tile<WM, WP, BC, 4>::NT,                                                                     \
+        reinterpret_cast<const void *>(&conv1x1_vec_kernel<WM, WP, BC, true, 4>),                          \
+        Vec1x1Tile<WM, WP, BC, 4>::MIN_BLOCKS, 1, Vec1x1Tile<WM, WP, BC, 4>::STAGES, 4                     \
   }
 // 4-byte staging variant for planes with H*W % 4 != 0 (kind 2)
 #define B2C_SCA1X1(NAME, WM, WP, BC)                                                                       \
@@ -88,6 +97,13 @@ const Family kFamilies[] = {
     B2C_VEC1X1("fused_1x1v_m64", 2, 4, 16),
     B2C_VEC1X1("fused_1x1v_m64p128", 2, 2, 16),
     B2C_VEC1X1("fused_1x1v_m128", 4, 2, 16),
+    B2C_VEC1X1("fused_1x1v_m32b32", 1, 4, 32),
+    B2C_VEC1X1("fused_1x1v_m64b32", 2, 4, 32),
+    B2C_VEC1X1("fused_1x1v_m128b32", 4, 2, 32),
+    B2C_VEC1X1W("fused_1x1w_m64", 1, 4, 16),
+    B2C_VEC1X1W("fused_1x1w_m128", 2, 2, 16),
+    B2C_VEC1X1W("fused_1x1w_m256", 4, 1, 16),
+    B2C_VEC1X1W("fused_1x1w_m128p256", 2, 4, 16),
     // pointwise, 4-byte pixel staging (1x1, stride 1, no padding, any H*W)
     // (and strided 1x1, e.g. ResNet projection shortcuts)
     B2C_SCA1X1("fused_1x1s_m32", 1, 4, 16),
@@ -217,7 +233,7 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
       const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
       tc.occupancy = std::max(1, std::min({f.max_ctas_per_sm, by_smem, 2048 / f.threads}));
       tc.ws_bytes = tc.splits > 1 ? 4LL * tc.splits * g.N * g.M * g.HoWo : 0;
-      tc.cost = model_cost(g, tc, 1, false, sms, tc.occupancy);
+      tc.cost = model_cost(g, tc, 1, false, sms, tc.occupancy) * (f.kind == 1 && f.tm == 2 ? 1.12 : 1.0);
       if (tc.cost < best.cost) {
         best.family = fam_id;
         best.tc = tc;
@@ -316,6 +332,26 @@ bool cluster_reduce_enabled() {
   static const bool on = false;
 #endif
   return on;
+}
+
+// Resident CTAs per SM of a kernel at a given dynamic shared memory size
+// (cached per family, size and device).
+int resident_ctas(int family, const void *kernel, int threads, int smem, int dev) {
+  static std::unordered_map<long long, int> cache;
+  const long long key = (((long long)family * 64 + dev) << 20) + smem;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, (size_t)smem) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 1;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  cache[key] = n;
+  return n;
 }
 
 const char *family_name(int id) {
@@ -504,6 +540,7 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   p.XCS = tc.xcs;
   p.vec_ok = ((long long)g.H * g.W % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   p.mtiles = (int)cdiv(g.M, tc.bm);
+  p.ptiles = (int)cdiv(g.Q, tc.bp);
   p.nchunks = (int)cdiv(g.C, tc.bc);
   p.splits = tc.splits;
   p.chunks_per_split = tc.splits > 1 ? tc.chunks_per_split : p.nchunks;
@@ -566,6 +603,19 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
       p.cluster = 1;
       smem = csmem;
     }
+  }
+  // pointwise kernels storing float4 outside a cluster: persistent grid of one
+  // wave of resident CTAs walking the work items (conv1x1_vec.cuh)
+  p.vec_out = (g.HoWo % 4 == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0) &&
+              (tc.splits <= 1 || ((reinterpret_cast<uintptr_t>(p.partials) & 15) == 0));
+  bool persist = f.kind == 1 && !p.cluster;
+#ifdef B2C_DEV
+  if (const char *e = std::getenv("B2C_PERSIST")) persist = !p.cluster && (f.kind == 1 || (f.kind == 2 && p.vec_out)) && std::atoi(e);
+#endif
+  if (persist) {
+    const long long items = tc.grid * tc.splits;
+    const long long slots = (long long)sm_count_of(dev) * resident_ctas(tc.family, f.kernel, tc.threads, smem, dev);
+    grid = dim3((unsigned)std::max<long long>(1, std::min(items, slots)), 1, 1);
   }
   void *args[] = {&p};
   note_launch();
