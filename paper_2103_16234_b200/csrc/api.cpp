@@ -394,6 +394,8 @@ b2c_status b2c_register_tuned_plan(const b2c_conv_desc *d, int32_t engine, int32
   if (!b2c::family_matches(family, g, stage1))
     return fail(B2C_INVALID_PLAN, "family %d cannot run this configuration", family);
   if (reduce < 0 || reduce > 2) return fail(B2C_INVALID_ARGUMENT, "reduce must be 0, 1 or 2, got %d", reduce);
+  if (reduce == 2 && !b2c::family_has_cluster_epilogue(family))
+    return fail(B2C_INVALID_PLAN, "family %s has no DSMEM cluster reduction", b2c::family_name(family));
   b2c::register_tuned(g, stage1, family, splits, reduce);
   std::lock_guard<std::mutex> lk(g_plan_mu);
   g_plans.clear();  // cached plans may predate the registration
@@ -419,14 +421,15 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
   st = get_tiles(d, g, false, forced, forced_splits, true, &tc, true, forced_reduce);
   if (st != B2C_OK) return st;
   const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
-                         reinterpret_cast<uintptr_t>(workspace)) & 15) == 0;
+                         reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(workspace)) & 15) == 0;
   const bool ws_ok = tc.splits <= 1 || (workspace && workspace_size >= tc.ws_bytes);
   if (!ws_ok && forced_splits > 1)
     return fail(B2C_INVALID_ARGUMENT, "split %d needs a %lld-byte workspace, %lld provided", forced_splits,
                 (long long)tc.ws_bytes, (long long)workspace_size);
-  if (tc.kind == 1 && !aligned && forced >= 0)
-    return fail(B2C_INVALID_ARGUMENT, "family %s needs 16-byte aligned x, y and workspace", b2c::family_name(forced));
-  if (!ws_ok || (tc.kind == 1 && !aligned)) {
+  const bool needs_align = tc.kind == 1;
+  if (needs_align && !aligned && forced >= 0)
+    return fail(B2C_INVALID_ARGUMENT, "family %s needs 16-byte aligned x, w, y and workspace", b2c::family_name(forced));
+  if (!ws_ok || (needs_align && !aligned)) {
     st = get_tiles(d, g, false, forced, ws_ok ? forced_splits : 0, ws_ok, &tc, aligned, forced_reduce);
     if (st != B2C_OK) return st;
   }

@@ -202,25 +202,33 @@ __device__ __forceinline__ void cluster_reduce_tile(const KParams &p, float *til
 }
 
 // HF_T/WF_T/S_T == 0 -> taken from the runtime parameters (generic family).
-template <int HF_T, int WF_T, int S_T, int BM, int BP, int BC, bool STRICT>
+// RP_ = output pixels per thread: 4 (64 accumulators, 2 CTAs of 256 threads per
+// SM) or 8 (128 accumulators, 128-thread CTAs).  Per (channel, tap) a thread
+// loads 16 filter values (4 LDS.128, warp-wide broadcast, 4 shared-memory
+// wavefronts each) and RP pixels (1 wavefront each) for 8*RP FFMA2: at RP = 4
+// that is 20 wavefronts per 64 FMA-pipe cycles of a warp, 80 % of the
+// 128 B/clk shared-memory rate at the FFMA2 peak with four warps per SMSP
+// (the measured ceiling of the 3x3 family, ~68 % FMA-pipe active); RP = 8
+// needs 24 per 128 cycles (75 % at peak).
+template <int HF_T, int WF_T, int S_T, int BM, int BP, int BC, bool STRICT, int RP_ = 4>
 struct ConvTile {
   static constexpr int RM = 16;
-  static constexpr int RP = 4;
+  static constexpr int RP = RP_;
   static constexpr int NTP = BP / RP;
   static constexpr int NMG = BM / RM;
   static constexpr int NT = NMG * NTP;
   static constexpr int WS = BM + 4;  // weight row stride: keeps LDS.128 alignment, spreads banks
   // target 16 resident warps per SM at <= 128 registers per thread
-  static constexpr int MIN_BLOCKS = NT >= 512 ? 1 : 512 / NT;
+  static constexpr int MIN_BLOCKS = RP_ == 4 ? (NT >= 512 ? 1 : 512 / NT) : (NT >= 256 ? 1 : 256 / NT);
   static_assert(BM % RM == 0, "BM must be a multiple of 16");
   static_assert(NTP % 32 == 0, "a warp must share one channel group");
 };
 
-template <int HF_T, int WF_T, int S_T, int BM, int BP, int BC, bool STRICT>
-__global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>::NT,
-                                  ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>::MIN_BLOCKS)
+template <int HF_T, int WF_T, int S_T, int BM, int BP, int BC, bool STRICT, int RP_ = 4>
+__global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT, RP_>::NT,
+                                  ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT, RP_>::MIN_BLOCKS)
     conv_direct_kernel(const KParams p) {
-  using T = ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT>;
+  using T = ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT, RP_>;
   constexpr int RM = T::RM, RP = T::RP, NTP = T::NTP, NT = T::NT, WS = T::WS;
   const int hf = HF_T ? HF_T : p.HF;
   const int wf = WF_T ? WF_T : p.WF;

@@ -47,6 +47,14 @@ struct Family {
         ConvTile<HF, WF, S, BM, BP, BC, STRICT>::MIN_BLOCKS, 0, 2                                          \
   }
 
+// 16 channels x 8 pixels per thread (conv_kernel.cuh ConvTile, RP = 8)
+#define B2C_FAMILY8(NAME, HF, WF, S, BM, BP, BC)                                                           \
+  Family {                                                                                                 \
+    NAME, HF, WF, S, BM, BP, BC, false, ConvTile<HF, WF, S, BM, BP, BC, false, 8>::NT,                    \
+        reinterpret_cast<const void *>(&conv_direct_kernel<HF, WF, S, BM, BP, BC, false, 8>),             \
+        ConvTile<HF, WF, S, BM, BP, BC, false, 8>::MIN_BLOCKS, 0, 2                                        \
+  }
+
 #define B2C_VEC1X1(NAME, WM, WP, BC)                                                                       \
   Family {                                                                                                 \
     NAME, 1, 1, 1, Vec1x1Tile<WM, WP, BC>::BM, Vec1x1Tile<WM, WP, BC>::BP, BC, false,                      \
@@ -82,6 +90,18 @@ const Family kFamilies[] = {
     B2C_FAMILY("fused_3x3s1_m64p128", 3, 3, 1, 64, 128, 8, false),
     B2C_FAMILY("fused_3x3s1_m64", 3, 3, 1, 64, 256, 8, false),
     B2C_FAMILY("fused_3x3s1_m128", 3, 3, 1, 128, 256, 8, false),
+    B2C_FAMILY8("fused_3x3s1_m64r8", 3, 3, 1, 64, 256, 8),
+    B2C_FAMILY8("fused_3x3s1_m32r8", 3, 3, 1, 32, 256, 8),
+    B2C_FAMILY8("fused_3x3s1_m64r8p512", 3, 3, 1, 64, 512, 8),
+    B2C_FAMILY8("fused_3x3s1_m128r8", 3, 3, 1, 128, 256, 8),
+    B2C_FAMILY8("fused_3x3s2_m64r8", 3, 3, 2, 64, 256, 8),
+    B2C_FAMILY8("fused_3x3s2_m128r8", 3, 3, 2, 128, 256, 8),
+    B2C_FAMILY8("fused_5x5s1_m64r8", 5, 5, 1, 64, 256, 4),
+    B2C_FAMILY8("fused_5x5s1_m32r8", 5, 5, 1, 32, 256, 4),
+    B2C_FAMILY8("fused_7x7s2_m32r8", 7, 7, 2, 32, 256, 4),
+    B2C_FAMILY8("fused_7x7s2_m64r8", 7, 7, 2, 64, 256, 4),
+    B2C_FAMILY("fused_7x7s2_m32", 7, 7, 2, 32, 256, 4, false),
+    B2C_FAMILY("fused_7x7s2_m64p128", 7, 7, 2, 64, 128, 4, false),
     B2C_FAMILY("fused_3x3s2_m64", 3, 3, 2, 64, 256, 8, false),
     B2C_FAMILY("fused_3x3s2_m128", 3, 3, 2, 128, 256, 8, false),
     B2C_FAMILY("fused_5x5s1_m32", 5, 5, 1, 32, 256, 4, false),
@@ -385,6 +405,10 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
 
 int device_sm_count(int device) { return sm_count_of(device); }
 
+bool family_has_cluster_epilogue(int fam_id) {
+  return fam_id >= 0 && fam_id < kNumFamilies && !kFamilies[fam_id].strict;
+}
+
 // Measured plans ("find" results of tools/autotune.py, registered at import by
 // the Python package): exact (shape, engine) -> (family, splits).
 struct TunedKey {
@@ -430,7 +454,7 @@ bool plan_tiles_core(const Geom &g, bool stage1, int device, int forced_family, 
       auto it = g_tuned.find(tuned_key(g, stage1));
       if (it != g_tuned.end()) t = it->second;
     }
-    if (t.family >= 0 && (allow_split || t.splits <= 1) && (allow_vec || kFamilies[t.family].kind == 0) &&
+    if (t.family >= 0 && (allow_split || t.splits <= 1) && (allow_vec || kFamilies[t.family].kind != 1) &&
         family_matches(t.family, g, stage1) &&
         evaluate(g, t.family, stage1, sms, t.splits, allow_split, &best)) {
       *out = best.tc;
@@ -608,9 +632,15 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   // wave of resident CTAs walking the work items (conv1x1_vec.cuh)
   p.vec_out = (g.HoWo % 4 == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0) &&
               (tc.splits <= 1 || ((reinterpret_cast<uintptr_t>(p.partials) & 15) == 0));
-  bool persist = f.kind == 1 && !p.cluster;
+  // Measured on B200 (profiles/ab/r2_persist_ab.txt): the persistent grid is
+  // 2-9 % SLOWER than one work item per CTA on every ResNet-50 / GoogLeNet
+  // pointwise layer — the hardware CTA scheduler balances the tail and keeps
+  // the channel tiles of a pixel tile co-resident (L2 reuse) better than a
+  // static item stride — so it stays a development option.
+  bool persist = false;
 #ifdef B2C_DEV
   if (const char *e = std::getenv("B2C_PERSIST")) persist = !p.cluster && (f.kind == 1 || (f.kind == 2 && p.vec_out)) && std::atoi(e);
+  if (std::getenv("B2C_KIND2_TRANSPOSE")) p.vec_out = 0;
 #endif
   if (persist) {
     const long long items = tc.grid * tc.splits;

@@ -63,6 +63,7 @@ const char *family_name(int id);
 int num_families();
 bool family_matches(int fam_id, const Geom &g, bool stage1);
 int device_sm_count(int device);
+bool family_has_cluster_epilogue(int fam_id);
 bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int forced_splits, bool allow_split,
                 bool allow_vec, TileChoice *out, int forced_reduce = 0);
 cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, const float *w, float *y,

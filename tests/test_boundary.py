@@ -426,7 +426,7 @@ def test_split_reduction_mode_plumbing():
     with pytest.raises(pk.ConvKitError):
         pk.select_tiles(cfg, splits=8, reduce=3)
     one = pk.ConvConfig("red1", n=3, c=520, h=14, w=14, m=130, hf=1, wf=1)
-    fam = pk.select_tiles(one, splits=4).family_id
+    fam = pk.select_tiles(one, splits=4, reduce=2).family_id
     lib = nat.lib()
     assert lib.b2c_register_tuned_plan(ctypes.byref(nat.desc(one)), nat.ENGINE_FUSED, fam, 4, 2) == nat.OK
     auto = pk.select_tiles(one)
