@@ -73,6 +73,10 @@ struct KParams {
   unsigned long long mRS, mHp, mHoWo, mWo;  // exact division magics: floor(2^44/d) + 1 (see fdiv)
   int pdl;                    // launched with programmatic dependent launch
   int cluster;                // split-C partials reduced through DSMEM: the splits of a tile form one cluster
+  int nb;                     // row-segment kernel (conv_row.cuh): segments per output row
+  int segs;                   // row-segment kernel: N*Ho*nb segments
+  int w_tma;                  // warp-specialised row kernel: filter tiles by 2-D TMA (tensor map argument)
+  unsigned long long spin_limit;  // mbarrier wait bound (ns) before __trap; 0 = unbounded (watchdog_ns())
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -201,6 +205,106 @@ __device__ __forceinline__ void cluster_reduce_tile(const KParams &p, float *til
   cluster_barrier();  // keep this CTA's tile alive until every rank has read it
 }
 
+// ---- halo staging, shared by the direct kernels ---------------------------------
+// A tile's receptive field is a band of ROWS "virtual rows" (row V = n*Hp +
+// padded y) of RC columns, staged per channel at shared position
+// shift + r*RS + col (RS == W mod 4, so every row is 16-byte congruent with its
+// global row).  goff[pos] = global element offset relative to image n0 channel
+// 0 (-1: zero padding, -2: unused slot); gtab[G] = offset of an aligned run of
+// 4 data elements for 16-byte group G, -1 for a mixed group (element-wise
+// copies), -3 for an all-unused group.  Built once per tile, reused for every
+// channel chunk.  Ends with a barrier (gtab reads goff).
+template <int NT>
+__device__ __forceinline__ void build_halo_tables(const KParams &p, int *goff, int *gtab, int vlo, int n0, int shift,
+                                                  int tap_x, long long chw) {
+  for (int pos = threadIdx.x; pos < p.XCS; pos += NT) {
+    const int rel = pos - shift;
+    int g = -2;
+    if (rel >= 0) {
+      const int r = fdiv(rel, p.mRS);
+      const int col = rel - r * p.RS;
+      if (r < p.ROWS && col < p.RC) {
+        const int vrel = vlo - n0 * p.Hp + r;  // virtual row relative to image n0 (< 2^20)
+        const int dn = fdiv(vrel, p.mHp);
+        const int n = n0 + dn;
+        const int iy = vrel - dn * p.Hp - p.PH;
+        const int ix = col + tap_x - p.PW;
+        const bool ok = (n < p.N) && (iy >= 0) && (iy < p.H) && (ix >= 0) && (ix < p.W);
+        g = ok ? (int)((long long)dn * chw + iy * p.W + ix) : -1;
+      }
+    }
+    goff[pos] = g;
+  }
+  __syncthreads();
+  const int ngroups = p.XCS >> 2;
+  for (int G = threadIdx.x; G < ngroups; G += NT) {
+    const int g0 = goff[4 * G], g1 = goff[4 * G + 1], g2 = goff[4 * G + 2], g3 = goff[4 * G + 3];
+    int t = -1;
+    if (p.vec_ok && g0 >= 0 && (g0 & 3) == 0 && g1 == g0 + 1 && g2 == g0 + 2 && g3 == g0 + 3) t = g0;
+    else if (g0 == -2 && g1 == -2 && g2 == -2 && g3 == -2) t = -3;
+    gtab[G] = t;
+  }
+}
+
+// Stage BC channel planes of the band (channel stride XCS floats) from xsrc =
+// &x[n0][c0][0][0]: 16-byte cp.async for aligned data runs, 4-byte copies and
+// (ZERO) +0.0 stores of the padding elsewhere; channels >= cvalid are left
+// untouched (never read).  Threads t0, t0 + tstride, ... of the CTA take part.
+template <int BC, bool ZERO = true>
+__device__ __forceinline__ void stage_halo_chunk(const KParams &p, const int *goff, const int *gtab, float *xs,
+                                                 const float *xsrc, int cvalid, int hw, int t0, int tstride) {
+  const int ngroups = p.XCS >> 2;
+  for (int G = t0; G < ngroups; G += tstride) {
+    const int t = gtab[G];
+    if (t == -3) continue;
+    float *dst = xs + 4 * G;
+    if (t >= 0) {
+      const float *src = xsrc + t;
+#pragma unroll
+      for (int c = 0; c < BC; c++) {
+        if (c < cvalid) cp_async16(dst, src);
+        dst += p.XCS;
+        src += hw;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int g = goff[4 * G + k];
+        float *d = dst + k;
+        if (g >= 0) {
+          const float *src = xsrc + g;
+          for (int c = 0; c < cvalid; c++, d += p.XCS, src += hw) cp_async4(d, src);
+        } else if (ZERO && g == -1) {
+          for (int c = 0; c < cvalid; c++, d += p.XCS) *d = 0.0f;
+        }
+      }
+    }
+  }
+}
+
+// Filters w[m0+m][c0+c][tap] -> ws[(c*taps + tap)*(BM+4) + m] (transposed, so
+// a thread's 16 output channels of one (channel, tap) are 4 LDS.128); wsrc =
+// &w[m0][c0][tap0]; per_m = BC*taps; taps past ct_valid and channels past M
+// are zero.
+template <int NT, int BM>
+__device__ __forceinline__ void stage_filter_chunk(const KParams &p, float *ws, const float *wsrc, int per_m, int taps,
+                                                   int ct_valid, bool w_dense, int m0) {
+  constexpr int WS = BM + 4;
+  const int wtotal = BM * per_m;
+  const int mstride = p.C * p.w_ctaps;
+  for (int e = threadIdx.x; e < wtotal; e += NT) {
+    const int m = e / per_m;
+    const int ct = e - m * per_m;
+    float *dst = ws + ct * WS + m;
+    if (m0 + m < p.M && ct < ct_valid) {
+      const int off = w_dense ? ct : (ct / taps) * p.w_ctaps + (ct % taps);
+      cp_async4(dst, wsrc + m * mstride + off);
+    } else {
+      *dst = 0.0f;
+    }
+  }
+}
+
 // HF_T/WF_T/S_T == 0 -> taken from the runtime parameters (generic family).
 // RP_ = output pixels per thread: 4 (64 accumulators, 2 CTAs of 256 threads per
 // SM) or 8 (128 accumulators, 128-thread CTAs).  Per (channel, tap) a thread
@@ -274,37 +378,7 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT, 
   // interior of every row can then move as 16-byte groups
   const int shift = (((vlo - n0 * p.Hp - p.PH) * p.W + tap_x - p.PW) % 4 + 4) % 4;
 
-  // ---- halo band: per shared position, the global offset (same for every
-  // channel): >= 0 data, -1 zero padding, -2 unused
-  for (int pos = tid; pos < p.XCS; pos += NT) {
-    const int rel = pos - shift;
-    int g = -2;
-    if (rel >= 0) {
-      const int r = fdiv(rel, p.mRS);
-      const int col = rel - r * p.RS;
-      if (r < p.ROWS && col < p.RC) {
-        const int vrel = vlo - n0 * p.Hp + r;  // virtual row relative to image n0 (< 2^20)
-        const int dn = fdiv(vrel, p.mHp);
-        const int n = n0 + dn;
-        const int iy = vrel - dn * p.Hp - p.PH;
-        const int ix = col + tap_x - p.PW;
-        const bool ok = (n < p.N) && (iy >= 0) && (iy < p.H) && (ix >= 0) && (ix < p.W);
-        g = ok ? (int)((long long)dn * chw + iy * p.W + ix) : -1;
-      }
-    }
-    goff[pos] = g;
-  }
-  __syncthreads();
-  // 16-byte groups: global offset of a contiguous aligned run of 4 data
-  // elements, -1 for a mixed group (element-wise path), -3 for all-unused
-  for (int G = tid; G < ngroups; G += NT) {
-    const int g0 = goff[4 * G], g1 = goff[4 * G + 1], g2 = goff[4 * G + 2], g3 = goff[4 * G + 3];
-    int t = -1;
-    if (p.vec_ok && g0 >= 0 && (g0 & 3) == 0 && g1 == g0 + 1 && g2 == g0 + 2 && g3 == g0 + 3) t = g0;
-    else if (g0 == -2 && g1 == -2 && g2 == -2 && g3 == -2) t = -3;
-    gtab[G] = t;
-  }
-
+  build_halo_tables<NT>(p, goff, gtab, vlo, n0, shift, tap_x, chw);
   // ---- per-thread output pixels: shared-memory offsets of their windows ----
   const long long trace_cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   int pix_off[RP];
@@ -328,53 +402,10 @@ __global__ void __launch_bounds__(ConvTile<HF_T, WF_T, S_T, BM, BP, BC, STRICT, 
   const bool w_dense = (p.w_ctaps == taps);  // fused: filter taps of a channel are contiguous
   auto load_chunk = [&](int chunk, float *stage) {
     const int c0 = chunk * BC;
-    float *xs = stage;
-    float *ws = stage + xfloats;
-    const float *xsrc = xtile + (long long)c0 * hw;
     const int cvalid = min(BC, p.C - c0);
-    for (int G = tid; G < ngroups; G += NT) {
-      const int t = gtab[G];
-      if (t == -3) continue;
-      float *dst = xs + 4 * G;
-      if (t >= 0) {
-        const float *src = xsrc + t;
-#pragma unroll
-        for (int c = 0; c < BC; c++) {
-          if (c < cvalid) cp_async16(dst, src);
-          dst += p.XCS;
-          src += hw;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-          const int g = goff[4 * G + k];
-          float *d = dst + k;
-          if (g >= 0) {
-            const float *src = xsrc + g;
-            for (int c = 0; c < cvalid; c++, d += p.XCS, src += hw) cp_async4(d, src);
-          } else if (g == -1) {
-            for (int c = 0; c < cvalid; c++, d += p.XCS) *d = 0.0f;
-          }
-        }
-      }
-    }
-    // filters: w[m0+m][c0 + c][tap] -> ws[(c*taps + tap)*WS + m]
-    const int per_m = BC * taps;
-    const int wtotal = BM * per_m;
-    const float *wsrc = p.w + ((long long)m0 * p.C + c0) * p.w_ctaps + w_tap0;
-    const int mstride = p.C * p.w_ctaps;
-    const int ct_valid = cvalid * taps;
-    for (int e = tid; e < wtotal; e += NT) {
-      const int m = e / per_m;
-      const int ct = e - m * per_m;
-      float *dst = ws + ct * WS + m;
-      if (m0 + m < p.M && ct < ct_valid) {
-        const int off = w_dense ? ct : (ct / taps) * p.w_ctaps + (ct % taps);
-        cp_async4(dst, wsrc + m * mstride + off);
-      } else {
-        *dst = 0.0f;
-      }
-    }
+    stage_halo_chunk<BC>(p, goff, gtab, stage, xtile + (long long)c0 * hw, cvalid, hw, threadIdx.x, NT);
+    stage_filter_chunk<NT, BM>(p, stage + xfloats, p.w + ((long long)m0 * p.C + c0) * p.w_ctaps + w_tap0, BC * taps,
+                               taps, cvalid * taps, w_dense, m0);
   };
 
   // ---- accumulators -------------------------------------------------------

@@ -7,6 +7,7 @@
 // pipeline stage) by minimising an occupancy- and wave-quantisation-aware cost
 // over the 148 SMs.  The reference plan is still computed and validated by the
 // C ABI for the drop-in's RunStats / InvalidPlan contract (api.cpp).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -20,7 +21,9 @@
 #include <cstdio>
 
 #include "conv1x1_vec.cuh"
+#include "conv1x1_ws.cuh"
 #include "conv_kernel.cuh"
+#include "conv_row.cuh"
 #include "internal.h"
 
 namespace b2c {
@@ -35,9 +38,13 @@ struct Family {
   int threads;
   const void *kernel;
   int max_ctas_per_sm;  // from __launch_bounds__
-  int kind;             // 0: conv_direct_kernel (halo staging), 1: conv1x1_vec_kernel, 2: its 4-byte variant
+  int kind;             // 0: conv_direct_kernel (halo staging), 1: conv1x1_vec_kernel, 2: its 4-byte variant,
+                        // 3: conv_row_kernel (row segments, halo staging), 4: its warp-specialised
+                        //    variant (producer warp, mbarrier ring, TMA filter tiles), 5: the
+                        //    warp-specialised pointwise kernel (conv1x1_ws.cuh, any stride)
   int stages;           // cp.async pipeline depth of kind 1
   int tm = 2;           // pointwise kernels: channel groups of 4 per thread (4: 16 channels x 8 pixels)
+  int rx = 0;           // kind 3: outputs per row segment
 };
 
 #define B2C_FAMILY(NAME, HF, WF, S, BM, BP, BC, STRICT)                                                    \
@@ -75,6 +82,33 @@ struct Family {
     NAME, 1, 1, 1, Vec1x1Tile<WM, WP, BC>::BM, Vec1x1Tile<WM, WP, BC>::BP, BC, false,                      \
         Vec1x1Tile<WM, WP, BC>::NT, reinterpret_cast<const void *>(&conv1x1_vec_kernel<WM, WP, BC, false>),\
         Vec1x1Tile<WM, WP, BC>::MIN_BLOCKS, 2, Vec1x1Tile<WM, WP, BC>::STAGES                              \
+  }
+
+// row-segment kernel (kind 3): 16 channels x RX outputs of one row per thread
+#define B2C_ROW(NAME, HF, WF, S, RX, WM, WP, BC, MINB)                                                    \
+  Family {                                                                                                 \
+    NAME, HF, WF, S, RowTile<HF, WF, S, RX, WM, WP, BC, MINB>::BM,                                         \
+        RowTile<HF, WF, S, RX, WM, WP, BC, MINB>::SEG * RX, BC, false,                                     \
+        RowTile<HF, WF, S, RX, WM, WP, BC, MINB>::NT,                                                      \
+        reinterpret_cast<const void *>(&conv_row_kernel<HF, WF, S, RX, WM, WP, BC, MINB>), MINB, 3, 2, 2, RX \
+  }
+
+// warp-specialised row-segment kernel (kind 4): ST-stage mbarrier ring, TMA filters
+#define B2C_ROWWS(NAME, HF, WF, S, RX, WM, WP, BC, ST)                                                    \
+  Family {                                                                                                 \
+    NAME, HF, WF, S, RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::BM,                                         \
+        RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::SEG * RX, BC, false,                                     \
+        RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,                                                      \
+        reinterpret_cast<const void *>(&conv_row_ws_kernel<HF, WF, S, RX, WM, WP, BC, ST>),                \
+        RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::MIN_BLOCKS, 4, ST, 2, RX                                  \
+  }
+
+// warp-specialised pointwise kernel (kind 5)
+#define B2C_PW1X1WS(NAME, WM, WP, BC, ST)                                                                   \
+  Family {                                                                                                 \
+    NAME, 1, 1, 1, Pw1x1WsTile<WM, WP, BC, ST>::BM, Pw1x1WsTile<WM, WP, BC, ST>::BP, BC, false,            \
+        Pw1x1WsTile<WM, WP, BC, ST>::NT, reinterpret_cast<const void *>(&conv1x1_ws_kernel<WM, WP, BC, ST>), \
+        Pw1x1WsTile<WM, WP, BC, ST>::MIN_BLOCKS, 5, ST, 4                                                   \
   }
 
 const Family kFamilies[] = {
@@ -133,6 +167,31 @@ const Family kFamilies[] = {
     // paper-faithful stage 1 (strict FMUL+FADD, one filter row per blockIdx.z)
     B2C_FAMILY("stage1_strict_m32", 1, 1, 1, 32, 256, 16, true),
     B2C_FAMILY("stage1_strict_m64", 1, 1, 1, 64, 256, 16, true),
+    // row-segment families (conv_row.cuh)
+    B2C_ROW("fused_3x3s1_row7_m64", 3, 3, 1, 7, 4, 1, 8, 3),
+    B2C_ROW("fused_3x3s1_row7_m64w2", 3, 3, 1, 7, 4, 2, 8, 1),
+    B2C_ROW("fused_3x3s1_row7_m128", 3, 3, 1, 7, 8, 1, 8, 1),
+    B2C_ROW("fused_3x3s1_row7_m32", 3, 3, 1, 7, 2, 2, 8, 3),
+    B2C_ROW("fused_3x3s2_row7_m64", 3, 3, 2, 7, 4, 1, 8, 3),
+    B2C_ROW("fused_3x3s2_row7_m128", 3, 3, 2, 7, 8, 1, 8, 1),
+    B2C_ROW("fused_5x5s1_row7_m64", 5, 5, 1, 7, 4, 1, 4, 3),
+    B2C_ROW("fused_5x5s1_row7_m32", 5, 5, 1, 7, 2, 2, 4, 3),
+    B2C_ROW("fused_7x7s2_row7_m64", 7, 7, 2, 7, 4, 1, 4, 2),
+    B2C_ROWWS("fused_3x3s1_rws7_m64", 3, 3, 1, 7, 4, 1, 8, 3),
+    B2C_ROWWS("fused_3x3s1_rws7_m64w2", 3, 3, 1, 7, 4, 2, 8, 4),
+    B2C_ROWWS("fused_3x3s1_rws7_m32", 3, 3, 1, 7, 2, 2, 8, 3),
+    B2C_ROWWS("fused_3x3s1_rws7_m128", 3, 3, 1, 7, 8, 1, 8, 3),
+    B2C_ROWWS("fused_3x3s2_rws7_m64", 3, 3, 2, 7, 4, 1, 8, 3),
+    B2C_ROWWS("fused_3x3s2_rws7_m128", 3, 3, 2, 7, 8, 1, 8, 3),
+    B2C_ROWWS("fused_5x5s1_rws7_m64", 5, 5, 1, 7, 4, 1, 4, 3),
+    B2C_ROWWS("fused_5x5s1_rws7_m32", 5, 5, 1, 7, 2, 2, 4, 3),
+    B2C_ROWWS("fused_7x7s2_rws7_m64", 7, 7, 2, 7, 4, 1, 4, 2),
+    // stride 2 on small planes: the band is ~2x the output rows, so 4-channel stages keep 2 CTAs per SM
+    B2C_ROWWS("fused_3x3s2_rws7_m64c4", 3, 3, 2, 7, 4, 1, 4, 3),
+    B2C_ROWWS("fused_3x3s2_rws7_m128c4", 3, 3, 2, 7, 8, 1, 4, 3),
+    // single-chunk layers (ResNet conv1, C = 3): one stage, two CTAs per SM
+    B2C_ROWWS("fused_7x7s2_rws7_m64st1", 7, 7, 2, 7, 4, 1, 4, 1),
+    B2C_ROWWS("fused_7x7s2_rws7_m32st1", 7, 7, 2, 7, 2, 2, 4, 1),
 };
 constexpr int kNumFamilies = sizeof(kFamilies) / sizeof(kFamilies[0]);
 
@@ -167,6 +226,58 @@ int max_tile_rows(const Geom &g, int hf_eff, int bp) {
   return worst;
 }
 
+// Row-segment kernel: rows of the virtual padded image stack spanned by the
+// worst tile of `seg` segments (nb segments per output row).
+int max_tile_rows_seg(const Geom &g, int nb, int seg) {
+  const long long segs = (long long)g.N * g.Ho * nb;
+  const long long tiles = cdiv(segs, seg);
+  int worst = 0;
+  for (long long t = 0; t < tiles; t++) {
+    const long long ra = t * seg / nb;
+    const long long rb = (std::min<long long>((t + 1) * seg, segs) - 1) / nb;
+    const long long va = (ra / g.Ho) * g.Hp + (ra % g.Ho) * g.S;
+    const long long vb = (rb / g.Ho) * g.Hp + (rb % g.Ho) * g.S;
+    worst = (int)std::max<long long>(worst, vb - va + g.HF);
+  }
+  return worst;
+}
+
+// Row stride of the row-segment kernel's band: >= rc, == W (mod 4) (16-byte
+// staging), and spreading the 32 segment origins of a warp over the 32 banks
+// (scalar pixel loads: one wavefront when all origins differ mod 32).  Scored
+// on the first warps of a sample of tiles.
+int pick_row_stride(const Geom &g, int rc, int nb, int rx, int seg) {
+  const long long segs = (long long)g.N * g.Ho * nb;
+  const long long tiles = cdiv(segs, seg);
+  int best_rs = rc + (((g.W - rc) % 4) + 4) % 4, best_score = INT_MAX;
+  for (int rs = best_rs; rs < best_rs + 64; rs += 4) {
+    int score = 0;
+    for (long long t = 0; t < std::min<long long>(tiles, 16); t++) {
+      const long long tt = t * std::max<long long>(1, tiles / 16);
+      const long long s0 = tt * seg;
+      const long long r0 = s0 / nb;
+      const long long v0 = (r0 / g.Ho) * g.Hp + (r0 % g.Ho) * g.S;
+      for (int w = 0; w < seg / 32; w++) {
+        int cnt[32] = {0};
+        int worst = 0;
+        for (int l = 0; l < 32; l++) {
+          const long long sg = std::min(s0 + 32 * w + l, segs - 1);
+          const long long r = sg / nb, b = sg - r * nb;
+          const long long v = (r / g.Ho) * g.Hp + (r % g.Ho) * g.S;
+          const int bank = (int)(((v - v0) * rs + b * rx * g.S) % 32);
+          worst = std::max(worst, ++cnt[bank]);
+        }
+        score += worst;
+      }
+    }
+    if (score < best_score) {
+      best_score = score;
+      best_rs = rs;
+    }
+  }
+  return best_rs;
+}
+
 struct Candidate {
   int family = -1;
   TileChoice tc;
@@ -182,9 +293,12 @@ double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, in
   // the halo-staged kernel on a 1x1 filter issues 4 LDS.128 + 4 LDS.32 per 32
   // FFMA2 against the pointwise kernels' 4 LDS.128 (measured: the pointwise
   // families win every 1x1 layer with H*W % 4 == 0 they can run, tuned_plans.json)
-  const double lds_penalty = (!stage1 && tc.kind == 0 && taps == 1) ? 1.25 : 1.0;
+  double lds_penalty = (!stage1 && tc.kind == 0 && taps == 1) ? 1.25 : 1.0;
+  // row segments: the FMA pipe, not the shared-memory crossbar, bounds them
+  if (tc.kind == 3) lds_penalty = 0.85;
+  if (tc.kind >= 4) lds_penalty = 0.8;  // no CTA-wide barriers in the channel loop
   const double fma = (double)tc.bm * tc.bp * taps * tc.bc * tc.chunks_per_split * (stage1 ? 2.0 : 1.0) * lds_penalty;
-  const double per_elem = (tc.kind == 1 || ((long long)g.H * g.W % 4 == 0 && tc.kind == 0)) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
+  const double per_elem = (tc.kind == 1 || (tc.kind == 5 && g.S == 1 && (long long)g.H * g.W % 4 == 0) || ((long long)g.H * g.W % 4 == 0 && (tc.kind == 0 || tc.kind >= 3))) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
   const double loads = (per_elem * tc.tile_elems + 4.0 * tc.bm * taps) * tc.bc * tc.chunks_per_split;
   const double fixed = 250000.0 + 12.0 * tc.tile_elems;
   const double split_io = tc.splits > 1 ? (double)tc.bm * tc.bp * 24.0 : 0.0;  // partial store per CTA
@@ -220,7 +334,7 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
   base.bc = f.bc;
   base.threads = f.threads;
   base.kind = f.kind;
-  if (f.kind >= 1) {
+  if (f.kind == 1 || f.kind == 2 || f.kind == 5) {
     base.rs = g.W;
     base.rows = 1;
     base.tile_elems = f.bp;
@@ -248,12 +362,15 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
       tc.stages = f.stages;
       long long smem = 4LL * f.stages * ((long long)f.bc * f.bp + (long long)f.bc * (f.bm + 4));
       if (f.kind == 2) smem = std::max(smem, 4LL * f.bm * f.bp);  // epilogue transposes the tile in smem
+      if (f.kind == 5)  // barriers | gather tables | ST x (filter tile | pixel tile)
+        smem = 128 + ((4LL * (f.bp + f.bp / 4) + 127) & ~127LL) + 4LL * f.stages * ((long long)f.bm * f.bc + (long long)f.bc * f.bp);
       if (smem > 226 * 1024) return false;
       tc.smem_bytes = (int)smem;
       const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
       tc.occupancy = std::max(1, std::min({f.max_ctas_per_sm, by_smem, 2048 / f.threads}));
       tc.ws_bytes = tc.splits > 1 ? 4LL * tc.splits * g.N * g.M * g.HoWo : 0;
       tc.cost = model_cost(g, tc, 1, false, sms, tc.occupancy) * (f.kind == 1 && f.tm == 2 ? 1.12 : 1.0);
+      if (f.kind == 5) tc.stages = f.stages;
       if (tc.cost < best.cost) {
         best.family = fam_id;
         best.tc = tc;
@@ -264,18 +381,31 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
     *out = best;
     return true;
   }
-  const int rc = (g.Wo - 1) * g.S + wf_eff;
-  base.rs = rc + (((g.W - rc) % 4) + 4) % 4;  // == W (mod 4): rows stay 16B-congruent with global rows
-  base.rows = max_tile_rows(g, hf_eff, f.bp);
+  long long ptiles;
+  if (f.kind == 3 || f.kind == 4) {
+    const int nb = (int)cdiv(g.Wo, f.rx);
+    const long long segs = (long long)g.N * g.Ho * nb;
+    const int seg = f.bp / f.rx;
+    if (segs + seg >= INT_MAX) return false;
+    const int rc = (nb * f.rx - 1) * g.S + g.WF;
+    base.rs = pick_row_stride(g, rc, nb, f.rx, seg);
+    base.rows = max_tile_rows_seg(g, nb, seg);
+    base.tile_elems = rc * base.rows;
+    ptiles = cdiv(segs, seg);
+  } else {
+    const int rc = (g.Wo - 1) * g.S + wf_eff;
+    base.rs = rc + (((g.W - rc) % 4) + 4) % 4;  // == W (mod 4): rows stay 16B-congruent with global rows
+    base.rows = max_tile_rows(g, hf_eff, f.bp);
+    base.tile_elems = rc * base.rows;
+    ptiles = cdiv(g.Q, f.bp);
+  }
   const long long positions = (long long)base.rs * base.rows + 3;
   if (positions > kFdivLimit || (long long)g.Hp + base.rows >= kFdivLimit) return false;
-  base.tile_elems = rc * base.rows;
   base.xcs = (int)((positions + 3) & ~3LL);
   // relative offsets inside a tile must fit int32 (goff table)
   const long long imgs = cdiv(f.bp, g.HoWo) + 2;
   if (imgs * (long long)g.C * g.H * g.W >= INT_MAX) return false;
   const long long mtiles = cdiv(g.M, f.bm);
-  const long long ptiles = cdiv(g.Q, f.bp);
   base.grid = mtiles * ptiles;
   base.grid_z = stage1 ? g.HF * g.WF : 1;
   const int nchunks = (int)cdiv(g.C, f.bc);
@@ -299,7 +429,13 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
     tc.stages = tc.chunks_per_split > 1 ? 2 : 1;
     const long long stage_floats = (long long)f.bc * tc.xcs + (long long)f.bc * taps * (f.bm + 4);
     const long long tables = tc.xcs + (((tc.xcs >> 2) + 3) & ~3);
-    const long long smem = 4LL * (tables + tc.stages * stage_floats);
+    long long smem = 4LL * (tables + tc.stages * stage_floats);
+    if (f.kind == 4) {  // conv_row_ws_kernel layout: barriers | tables | ST x (filter tile | band)
+      tc.stages = f.stages;
+      const long long wfloats = (long long)f.bm * f.bc * taps;
+      const long long xfl = ((long long)f.bc * tc.xcs + 31) & ~31LL;
+      smem = 128 + ((4LL * (tc.xcs + (tc.xcs >> 2)) + 127) & ~127LL) + 4LL * f.stages * (wfloats + xfl);
+    }
     if (smem > 226 * 1024) return best.family >= 0 ? (*out = best, true) : false;
     tc.smem_bytes = (int)smem;
     const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
@@ -399,6 +535,11 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
     return g.HF == 1 && g.WF == 1 && g.PH == 0 && g.PW == 0 && (g.S != 1 || ((long long)g.H * g.W) % 4 != 0) &&
            (long long)g.N * g.C * g.H * g.W < (1LL << 31);
   if (stage1) return g.S == 1;
+  if (f.kind == 3 || f.kind == 4)
+    return f.hf == g.HF && f.wf == g.WF && f.s == g.S && (long long)g.N * g.Ho * g.Wo < (1LL << 30);
+  if (f.kind == 5)  // gather offsets relative to a tile's first image stay in int32
+    return g.HF == 1 && g.WF == 1 && g.PH == 0 && g.PW == 0 &&
+           (cdiv(f.bp, g.HoWo) + 2) * (long long)g.C * g.H * g.W < INT_MAX;
   if (f.hf == 0) return true;  // generic
   return f.hf == g.HF && f.wf == g.WF && f.s == g.S;
 }
@@ -406,7 +547,7 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
 int device_sm_count(int device) { return sm_count_of(device); }
 
 bool family_has_cluster_epilogue(int fam_id) {
-  return fam_id >= 0 && fam_id < kNumFamilies && !kFamilies[fam_id].strict;
+  return fam_id >= 0 && fam_id < kNumFamilies && !kFamilies[fam_id].strict && kFamilies[fam_id].kind < 3;
 }
 
 // Measured plans ("find" results of tools/autotune.py, registered at import by
@@ -499,7 +640,7 @@ bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int f
   int r = 0;
   if (out->splits > 1 && !stage1) {
     r = forced_reduce > 0 ? forced_reduce : (tuned_reduce > 0 ? tuned_reduce : (cluster_reduce_enabled() ? 2 : 1));
-    if (r == 2 && out->splits > 16) {
+    if (r == 2 && (out->splits > 16 || !family_has_cluster_epilogue(out->family))) {
       if (forced_reduce == 2) return false;
       r = 1;
     }
@@ -515,6 +656,37 @@ bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int f
     }
   }
   return true;
+}
+
+// 2-D tensor map of the filter bank viewed as [M][C*hf*wf] (row-major, fp32)
+// for conv_row_ws_kernel's per-stage TMA tile {BC*hf*wf, BM}.  false when TMA
+// cannot address it (row pitch not a multiple of 16 bytes, unaligned base, a
+// box dimension above 256): the kernel then stages filters by cp.async.
+bool encode_filter_map(CUtensorMap *map, const Geom &g, const float *w, int bm, int bc) {
+  using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<EncodeFn>(fn);
+  }();
+  const long long row = (long long)g.C * g.HF * g.WF;
+  const int box0 = bc * g.HF * g.WF;
+  if (!encode || (row * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(w) & 15) != 0 || box0 > 256 || bm > 256 ||
+      (box0 * 4) % 16 != 0)
+    return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)row, (cuuint64_t)g.M};
+  const cuuint64_t strides[1] = {(cuuint64_t)(row * 4)};
+  const cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)bm};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(w), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, const float *w, float *y,
@@ -560,11 +732,20 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   p.Q = (int)g.Q;
   p.RS = tc.rs;
   p.RC = (g.Wo - 1) * g.S + (stage1 ? 1 : g.WF);
+  CUtensorMap wmap;
+  std::memset(&wmap, 0, sizeof(wmap));
+  if (f.kind == 4 || f.kind == 5) p.w_tma = encode_filter_map(&wmap, g, w, tc.bm, tc.bc) ? 1 : 0;
+  p.spin_limit = watchdog_ns();
+  if (f.kind == 3 || f.kind == 4) {
+    p.nb = (int)cdiv(g.Wo, f.rx);
+    p.segs = (int)((long long)g.N * g.Ho * p.nb);
+    p.RC = (p.nb * f.rx - 1) * g.S + g.WF;
+  }
   p.ROWS = tc.rows;
   p.XCS = tc.xcs;
   p.vec_ok = ((long long)g.H * g.W % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   p.mtiles = (int)cdiv(g.M, tc.bm);
-  p.ptiles = (int)cdiv(g.Q, tc.bp);
+  p.ptiles = (int)(tc.grid / p.mtiles);
   p.nchunks = (int)cdiv(g.C, tc.bc);
   p.splits = tc.splits;
   p.chunks_per_split = tc.splits > 1 ? tc.chunks_per_split : p.nchunks;
@@ -647,7 +828,7 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
     const long long slots = (long long)sm_count_of(dev) * resident_ctas(tc.family, f.kernel, tc.threads, smem, dev);
     grid = dim3((unsigned)std::max<long long>(1, std::min(items, slots)), 1, 1);
   }
-  void *args[] = {&p};
+  void *args[] = {&p, &wmap};  // the second is read by kind 4 only
   note_launch();
   cudaError_t err;
   if (p.pdl || p.cluster) {

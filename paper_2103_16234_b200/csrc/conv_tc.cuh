@@ -50,6 +50,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "ptx.cuh"
+
 namespace b2c {
 namespace tc {
 
@@ -101,61 +103,7 @@ struct TcParams {
 #endif
 
 // ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// mbarrier wait.  limit_ns == 0 (default): unbounded — a correct kernel may be
-// preempted or time-sliced for any length of time.  limit_ns > 0 (watchdog,
-// B2C_WATCHDOG_MS, set by the test suite): a protocol bug traps (kernel error)
-// instead of hanging the GPU; wall time (globaltimer), checked every 256 polls.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, unsigned long long limit_ns,
-                                          unsigned int *dbg = nullptr, unsigned code = 0) {
-  unsigned long long t0 = 0;
-  unsigned n = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if (limit_ns && (++n & 255u) == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t0 == 0) {
-        t0 = t;
-      } else if (t - t0 > limit_ns) {
-        if (dbg) atomicExch(dbg, code);
-        __threadfence_system();
-        __trap();
-      }
-    }
-  }
-}
-
-// One lane of a converged warp (elect.sync): the warp runs the role's loop
-// together so descriptors and loop state stay warp-uniform (uniform
-// datapath), and the elected lane issues the single-thread tcgen05 / bulk ops.
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
-      : "=r"(pred));
-  return pred != 0;
-}
+// smem_u32, mbarrier helpers and elect_one: ptx.cuh
 
 __device__ __forceinline__ void sts32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");

@@ -82,6 +82,9 @@ def main():
     ap.add_argument("--budget-s", type=float, default=1500)
     ap.add_argument("--engines", default="fused", help="comma list of fused, tf32x3, tf32")
     ap.add_argument("--batches", default="", help="override the batch sizes per workload (comma list)")
+    ap.add_argument("--all-records", action="store_true",
+                    help="write every tuned layer (keep=false where the cost model's plan won) for tools/merge_plans.py")
+    ap.add_argument("--layers", default="", help="only these layer names (comma list)")
     args = ap.parse_args()
     engines = args.engines.split(",")
     names = family_names()
@@ -92,7 +95,7 @@ def main():
         for n in batches:
             for cfg in W.layers(wl, n):
                 key = cfg.as_tuple()
-                if key in seen:
+                if key in seen or (args.layers and cfg.name not in args.layers.split(",")):
                     continue
                 seen.add(key)
                 if time.time() - t_start > args.budget_s:
@@ -127,8 +130,9 @@ def main():
                 rec = {"layer": f"{wl}/{cfg.name}/N{n}", "desc": list(key), "engine": "fused",
                        "family": best[1], "splits": best[2], "reduce": best[3], "us": round(best[0], 2),
                        "model_us": round(t_auto, 2)}
+                rec["keep"] = best[0] < t_auto * 0.97
                 print(json.dumps(rec), flush=True)
-                if best[0] < t_auto * 0.97:
+                if rec["keep"] or args.all_records:
                     plans.append(rec)
                 del x, w, y
                 torch.cuda.empty_cache()
