@@ -192,6 +192,10 @@ const Family kFamilies[] = {
     // single-chunk layers (ResNet conv1, C = 3): one stage, two CTAs per SM
     B2C_ROWWS("fused_7x7s2_rws7_m64st1", 7, 7, 2, 7, 4, 1, 4, 1),
     B2C_ROWWS("fused_7x7s2_rws7_m32st1", 7, 7, 2, 7, 2, 2, 4, 1),
+    // persistent warp-specialised pointwise families (conv1x1_ws.cuh)
+    B2C_PW1X1WS("fused_1x1ws_m64", 4, 2, 16, 4),
+    B2C_PW1X1WS("fused_1x1ws_m128", 8, 1, 16, 4),
+    B2C_PW1X1WS("fused_1x1ws_m32", 2, 4, 16, 3),
 };
 constexpr int kNumFamilies = sizeof(kFamilies) / sizeof(kFamilies[0]);
 
@@ -308,7 +312,9 @@ double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, in
   const double warps = tc.threads / 32.0;
   auto eff = [&](int k) { return std::min(1.0, k * warps / 12.0); };
   double t;
-  if (ctas <= (long long)sms * occ) {
+  if (tc.kind == 5) {  // persistent: one CTA per SM walks the items, no per-item pipeline fill
+    t = (fma + loads + split_io) * (double)cdiv(ctas, sms) + fixed;
+  } else if (ctas <= (long long)sms * occ) {
     const int k = (int)cdiv(ctas, sms);
     t = work * k / eff(k);
   } else {
@@ -362,8 +368,8 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
       tc.stages = f.stages;
       long long smem = 4LL * f.stages * ((long long)f.bc * f.bp + (long long)f.bc * (f.bm + 4));
       if (f.kind == 2) smem = std::max(smem, 4LL * f.bm * f.bp);  // epilogue transposes the tile in smem
-      if (f.kind == 5)  // barriers | gather tables | ST x (filter tile | pixel tile)
-        smem = 128 + ((4LL * (f.bp + f.bp / 4) + 127) & ~127LL) + 4LL * f.stages * ((long long)f.bm * f.bc + (long long)f.bc * f.bp);
+      if (f.kind == 5)  // barriers | ST x (filter tile | pixel tile)
+        smem = 128 + 4LL * f.stages * ((long long)f.bm * f.bc + (long long)f.bc * f.bp);
       if (smem > 226 * 1024) return false;
       tc.smem_bytes = (int)smem;
       const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
@@ -823,7 +829,9 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   if (const char *e = std::getenv("B2C_PERSIST")) persist = !p.cluster && (f.kind == 1 || (f.kind == 2 && p.vec_out)) && std::atoi(e);
   if (std::getenv("B2C_KIND2_TRANSPOSE")) p.vec_out = 0;
 #endif
-  if (persist) {
+  if (f.kind == 5) {  // persistent: one CTA per SM walks the (split, tile) items
+    grid = dim3((unsigned)std::max<long long>(1, std::min<long long>(tc.grid * tc.splits, sm_count_of(dev))), 1, 1);
+  } else if (persist) {
     const long long items = tc.grid * tc.splits;
     const long long slots = (long long)sm_count_of(dev) * resident_ctas(tc.family, f.kernel, tc.threads, smem, dev);
     grid = dim3((unsigned)std::max<long long>(1, std::min(items, slots)), 1, 1);

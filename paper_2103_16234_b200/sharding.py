@@ -36,14 +36,22 @@ def shard_config(cfg: ConvConfig, world: int, rank: int) -> ConvConfig:
     return cfg.with_batch(max(hi - lo, 0)) if hi > lo else cfg.with_batch(1)
 
 
+def _split_bounds(layer, c: int) -> tuple:
+    """First input channel of each split range of a fused plan."""
+    bc, splits = int(layer._tiles.bc), int(layer.splits)
+    per = -(-(-(-c // bc)) // splits) * bc  # chunks per split x channels per chunk
+    return tuple(min(c, s * per) for s in range(splits))
+
+
 def shard_layer(cfg: ConvConfig, local_cfg: ConvConfig, engine: str = "fused"):
     """The ConvLayer a rank runs for its slab ``local_cfg`` of the global
     layer ``cfg``, with the summation-order fields of its plan pinned to the
-    global plan (fused: split-C count; tensor core: A-operand mode and
-    split-K count), so its outputs do not depend on the world size.  The
-    slab's own plan (measured registry or planner) is kept whenever it already
-    agrees; otherwise its kernel family / filters-per-tile are kept and only
-    the order-relevant fields are forced."""
+    global plan (fused: the channel ranges of the split-C reduction, set by
+    the split count and the kernel family's channels per chunk; tensor core:
+    A-operand mode and split-K count), so its outputs do not depend on the
+    world size.  The slab's own plan (measured registry or planner) is kept
+    whenever it already agrees; otherwise its kernel family (else the global
+    plan's) is kept and only the order-relevant fields are forced."""
     from .engine import ConvLayer
     from .errors import InvalidPlan
 
@@ -52,13 +60,19 @@ def shard_layer(cfg: ConvConfig, local_cfg: ConvConfig, engine: str = "fused"):
         return local
     ref = ConvLayer(cfg, engine)
     if engine == "fused":
-        if local.splits == ref.splits:
+        # the summation order is fixed by the channel ranges of the splits,
+        # which follow from (splits, channels per pipeline chunk)
+        if _split_bounds(local, cfg.c) == _split_bounds(ref, cfg.c):
             return local
         reduce = ref.reduce if ref.splits > 1 else 0
-        try:
-            return ConvLayer(local_cfg, engine, family=int(local._tiles.family), splits=ref.splits, reduce=reduce)
-        except InvalidPlan:
-            return ConvLayer(local_cfg, engine, splits=ref.splits, reduce=reduce)
+        for fam in (int(local._tiles.family), int(ref._tiles.family)):
+            try:
+                cand = ConvLayer(local_cfg, engine, family=fam, splits=ref.splits, reduce=reduce)
+            except InvalidPlan:
+                continue
+            if _split_bounds(cand, cfg.c) == _split_bounds(ref, cfg.c):
+                return cand
+        raise InvalidPlan(f"no plan for the {local_cfg.n}-image shard reproduces the channel split of {cfg.name}")
     if local.splits == ref.splits and int(local._tc.mode) == int(ref._tc.mode):
         return local
     try:
