@@ -300,7 +300,10 @@ double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, in
   double lds_penalty = (!stage1 && tc.kind == 0 && taps == 1) ? 1.25 : 1.0;
   // row segments: the FMA pipe, not the shared-memory crossbar, bounds them
   if (tc.kind == 3) lds_penalty = 0.85;
-  if (tc.kind >= 4) lds_penalty = 0.8;  // no CTA-wide barriers in the channel loop
+  if (tc.kind == 4) lds_penalty = 0.8;  // no CTA-wide barriers in the channel loop
+  // persistent pointwise: measured on par with the 16-byte pointwise families on
+  // stride-1 planes, ahead on strided / 4-byte-staged ones (profiles/ab/r2_pointwise_ws_ab.txt)
+  if (tc.kind == 5) lds_penalty = (g.S == 1 && (long long)g.H * g.W % 4 == 0) ? 1.15 : 0.9;
   const double fma = (double)tc.bm * tc.bp * taps * tc.bc * tc.chunks_per_split * (stage1 ? 2.0 : 1.0) * lds_penalty;
   const double per_elem = (tc.kind == 1 || (tc.kind == 5 && g.S == 1 && (long long)g.H * g.W % 4 == 0) || ((long long)g.H * g.W % 4 == 0 && (tc.kind == 0 || tc.kind >= 3))) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
   const double loads = (per_elem * tc.tile_elems + 4.0 * tc.bm * taps) * tc.bc * tc.chunks_per_split;
@@ -591,7 +594,7 @@ void register_tuned(const Geom &g, bool stage1, int family, int splits, int redu
 // Planner: returns false if no family can run the geometry.
 namespace {
 bool plan_tiles_core(const Geom &g, bool stage1, int device, int forced_family, int forced_splits, bool allow_split,
-                     bool allow_vec, TileChoice *out, int *tuned_reduce) {
+                     bool allow_vec, TileChoice *out, int *tuned_reduce, bool need_cluster) {
   const int sms = sm_count_of(device);
   Candidate best;
   if (forced_family < 0 && forced_splits <= 0) {
@@ -602,6 +605,7 @@ bool plan_tiles_core(const Geom &g, bool stage1, int device, int forced_family, 
       if (it != g_tuned.end()) t = it->second;
     }
     if (t.family >= 0 && (allow_split || t.splits <= 1) && (allow_vec || kFamilies[t.family].kind != 1) &&
+        (!need_cluster || family_has_cluster_epilogue(t.family)) &&
         family_matches(t.family, g, stage1) &&
         evaluate(g, t.family, stage1, sms, t.splits, allow_split, &best)) {
       *out = best.tc;
@@ -620,6 +624,7 @@ bool plan_tiles_core(const Geom &g, bool stage1, int device, int forced_family, 
       const Family &f = kFamilies[i];
       if (!family_matches(i, g, stage1)) continue;
       if (!allow_vec && f.kind == 1) continue;
+      if (need_cluster && !family_has_cluster_epilogue(i)) continue;
       const bool generic = (f.hf == 0) && !stage1;
       if ((pass == 0) == generic) continue;  // specialised families first
       Candidate c;
@@ -641,7 +646,8 @@ bool plan_tiles_core(const Geom &g, bool stage1, int device, int forced_family, 
 bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int forced_splits, bool allow_split,
                 bool allow_vec, TileChoice *out, int forced_reduce) {
   int tuned_reduce = 0;
-  if (!plan_tiles_core(g, stage1, device, forced_family, forced_splits, allow_split, allow_vec, out, &tuned_reduce))
+  if (!plan_tiles_core(g, stage1, device, forced_family, forced_splits, allow_split, allow_vec, out, &tuned_reduce,
+                       forced_reduce == 2 && forced_family < 0))
     return false;
   int r = 0;
   if (out->splits > 1 && !stage1) {

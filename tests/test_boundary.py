@@ -247,7 +247,12 @@ def test_tile_planner_covers_every_baseline_layer(native):
                 t = pk.select_tiles(cfg)
                 ho, wo = pk.output_dims(cfg)
                 assert t.smem_bytes <= 227 * 1024
-                tiles = -(-cfg.m // t.bm) * -(-(cfg.n * ho * wo) // t.bp)
+                if "_row7_" in t.family or "_rws7_" in t.family:
+                    # row-segment kernels: tiles of bp/7 segments of 7 outputs of one row
+                    segs = cfg.n * ho * -(-wo // 7)
+                    tiles = -(-cfg.m // t.bm) * -(-segs // (t.bp // 7))
+                else:
+                    tiles = -(-cfg.m // t.bm) * -(-(cfg.n * ho * wo) // t.bp)
                 assert t.grid == tiles * t.splits, (wl, cfg.name)
                 chunks = -(-cfg.c // t.bc)
                 assert 1 <= t.splits <= chunks
