@@ -85,6 +85,8 @@ def main():
     ap.add_argument("--all-records", action="store_true",
                     help="write every tuned layer (keep=false where the cost model's plan won) for tools/merge_plans.py")
     ap.add_argument("--layers", default="", help="only these layer names (comma list)")
+    ap.add_argument("--families", default="", help="only fused families whose name contains one of these (comma list)")
+    ap.add_argument("--splits", default="1,2,3,4,6,8,12,16,24", help="fused split counts to try")
     args = ap.parse_args()
     engines = args.engines.split(",")
     names = family_names()
@@ -116,7 +118,9 @@ def main():
                 t_auto = time_layer(auto, x, w, y)
                 best = (t_auto, names[auto._tiles.family], auto.splits, auto.reduce)
                 for f in matching_families(cfg):
-                    for sp in (1, 2, 3, 4, 6, 8, 12, 16, 24):
+                    if args.families and not any(k in names[f] for k in args.families.split(",")):
+                        continue
+                    for sp in (int(v) for v in args.splits.split(",")):
                         for red in ((0,) if sp == 1 else (1, 2) if sp <= 16 else (1,)):
                             try:
                                 L = ConvLayer(cfg, family=f, splits=sp, reduce=red)
