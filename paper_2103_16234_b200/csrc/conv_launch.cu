@@ -192,12 +192,6 @@ const Family kFamilies[] = {
     // single-chunk layers (ResNet conv1, C = 3): one stage, two CTAs per SM
     B2C_ROWWS("fused_7x7s2_rws7_m64st1", 7, 7, 2, 7, 4, 1, 4, 1),
     B2C_ROWWS("fused_7x7s2_rws7_m32st1", 7, 7, 2, 7, 2, 2, 4, 1),
-    // row segments on pointwise layers: 7x7 planes (no 16-byte pixel groups for the
-    // flattened kernels) and strided projection shortcuts
-    B2C_ROWWS("fused_1x1s1_rws7_m64", 1, 1, 1, 7, 4, 1, 16, 4),
-    B2C_ROWWS("fused_1x1s1_rws7_m128", 1, 1, 1, 7, 8, 1, 16, 3),
-    B2C_ROWWS("fused_1x1s2_rws7_m64", 1, 1, 2, 7, 4, 1, 8, 3),
-    B2C_ROWWS("fused_1x1s2_rws7_m128", 1, 1, 2, 7, 8, 1, 8, 3),
     // persistent warp-specialised pointwise families (conv1x1_ws.cuh)
     B2C_PW1X1WS("fused_1x1ws_m64", 4, 2, 16, 4),
     B2C_PW1X1WS("fused_1x1ws_m128", 8, 1, 16, 4),

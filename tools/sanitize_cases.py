@@ -1,6 +1,7 @@
 """Small launches of every kernel kind, for compute-sanitizer (memcheck,
 racecheck, synccheck, initcheck): every fused family (halo-staged direct,
-16-byte and 4-byte pointwise), split-C through partial planes + stage 2 and
+row-segment and its warp-specialised TMA variant, 16-byte, 4-byte and
+persistent warp-specialised pointwise), split-C through partial planes + stage 2 and
 through DSMEM clusters, the paper-faithful stage 1 + stage 2, and the tcgen05
 engines in halo and gather mode (3xTF32 with bf16 corrections, TF32).
 Each result is checked against the oracle so a sanitizer run is also a
@@ -38,7 +39,10 @@ def main():
         ref = oracle.conv_f64(cfg, xn, wn)
         tol = oracle.fp32_tolerance(cfg.c, cfg.hf, cfg.wf)
         fams = pk.matching_families(cfg)
-        for fam in (fams[:2] if quick else fams):
+        if quick:  # two round-1 families plus every row-segment / warp-specialised one
+            names = pk.family_names()
+            fams = fams[:2] + [f for f in fams[2:] if any(k in names[f] for k in ("row7", "rws7", "1x1ws"))]
+        for fam in fams:
             for splits, reduce in ((1, 0), (2, 1), (2, 2)):
                 try:
                     layer = pk.ConvLayer(cfg, family=fam, splits=splits, reduce=reduce)
