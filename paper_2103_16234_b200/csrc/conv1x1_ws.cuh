@@ -28,9 +28,10 @@
 //            filters (4-byte cp.async when C*4 is not 16-byte aligned) and the
 //            pixel tile [BC][BP] by 16-byte cp.async (H*W % 4 == 0, stride 1)
 //            or 4-byte cp.async (7x7 planes, strided projection shortcuts),
-//            completion handed to the stage's full mbarrier
-//            (cp.async.mbarrier.arrive.noinc); consumers release a stage
-//            through its empty mbarrier.  No CTA-wide barrier after setup.
+//            each producer thread hands the completion of its copies of a stage
+//            to the stage's full mbarrier (cp.async.mbarrier.arrive.noinc);
+//            consumers release a stage for refill through a
+//            named barrier (arrive without waiting; the producers sync on it).  No CTA-wide barrier after setup.
 //   registers = 12 warps launch at 168 (the whole file); the producer
 //            warpgroup drops to 40 (setmaxnreg.dec) and the consumers rise to
 //            232 (setmaxnreg.inc) for their 128 accumulators.
@@ -62,6 +63,7 @@ struct Pw1x1WsTile {
   static constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232;
   static constexpr int GPT = (BP / 4 + NPT - 1) / NPT;  // 4-pixel groups per producer thread
   static_assert(NCW == 8, "two consumer warpgroups");
+  static_assert(ST >= 1 && ST <= 15, "one named barrier per stage (ids 1..ST)");
   static_assert(WFLOATS % 32 == 0, "stages must stay 128-byte aligned");
 };
 
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(Pw1x1WsTile<WM, WP, BC, ST>::NT, 1)
   constexpr int WFLOATS = T::WFLOATS, STAGE_FLOATS = T::STAGE_FLOATS;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);  // full[ST] | empty[ST]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);  // full[ST]
   float *stages = reinterpret_cast<float *>(smem_raw + 128);
 
   const int tid = threadIdx.x;
@@ -82,14 +84,20 @@ __global__ void __launch_bounds__(Pw1x1WsTile<WM, WP, BC, ST>::NT, 1)
   const long long items = tiles * p.splits;
   if (tid == 0) {
     for (int s = 0; s < ST; s++) {
-      mbar_init(smem_u32(&bars[s]), T::NPT);     // producer threads' cp.async arrivals (+ TMA bytes)
-      mbar_init(smem_u32(&bars[ST + s]), NCW);   // one arrival per consumer warp
+      mbar_init(smem_u32(&bars[s]), T::NPT);     // producer threads' arrivals (+ TMA bytes)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
 
+  // chunks this CTA walks over all its items: a stage is released for refill
+  // (named barrier 1 + s) only if a later chunk reuses it
+  long long total = 0;
+  for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+    const int sp = (int)(it / tiles);
+    total += min(p.nchunks, (sp + 1) * p.chunks_per_split) - sp * p.chunks_per_split;
+  }
   auto decode = [&](long long it, int &m0, long long &q0, int &cb, int &ce, int &split) {
     split = (int)(it / tiles);
     const long long t = it - (long long)split * tiles;
@@ -139,7 +147,7 @@ __global__ void __launch_bounds__(Pw1x1WsTile<WM, WP, BC, ST>::NT, 1)
         const int s = (int)(gi % ST);
         const long long kk = gi / ST;
         const uint32_t full = smem_u32(&bars[s]);
-        if (kk > 0) mbar_wait(smem_u32(&bars[ST + s]), (int)((kk - 1) & 1), p.spin_limit);
+        if (kk > 0) named_bar_sync(1 + s, T::NT);  // every consumer is done with the stage's previous chunk
         float *wst = stages + s * STAGE_FLOATS;
         const int c0 = chunk * BC;
         const int cvalid = min(BC, p.C - c0);
@@ -170,7 +178,7 @@ __global__ void __launch_bounds__(Pw1x1WsTile<WM, WP, BC, ST>::NT, 1)
                   cp_async4(xst + c * BP + e, xsrc + off[k][e] + (long long)c * in_hw);
           }
         }
-        cp_async_mbar_arrive_noinc(full);
+        cp_async_mbar_arrive_noinc(full);  // the arrive fires when this thread's copies have landed
       }
     }
     if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -218,8 +226,7 @@ __global__ void __launch_bounds__(Pw1x1WsTile<WM, WP, BC, ST>::NT, 1)
 #pragma unroll
           for (int j = 0; j < 8; j++) acc[r][j] = __ffma2_rn(w2[r], make_float2(xv[j], xv[j]), acc[r][j]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&bars[ST + s]));
+      if (gi + ST < total) named_bar_arrive(1 + s, T::NT);  // release the stage for refill
     }
 
     // ---- epilogue of this item (the producers are already filling the next) ----

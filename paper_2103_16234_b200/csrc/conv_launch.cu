@@ -195,7 +195,6 @@ const Family kFamilies[] = {
     // persistent warp-specialised pointwise families (conv1x1_ws.cuh)
     B2C_PW1X1WS("fused_1x1ws_m64", 4, 2, 16, 4),
     B2C_PW1X1WS("fused_1x1ws_m128", 8, 1, 16, 4),
-    B2C_PW1X1WS("fused_1x1ws_m32", 2, 4, 16, 3),
 };
 constexpr int kNumFamilies = sizeof(kFamilies) / sizeof(kFamilies[0]);
 

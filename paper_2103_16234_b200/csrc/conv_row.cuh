@@ -195,15 +195,18 @@ __global__ void __launch_bounds__(RowTile<HF, WF, S, RX, WM, WP, BC, MINB>::NT, 
 // Warp-specialised row-segment kernel (kind 4).  Same mapping and arithmetic
 // order as conv_row_kernel (bitwise identical for equal splits), but the CTA
 // never stops at a CTA-wide barrier inside the channel loop: WM*WP consumer
-// warps only compute, one producer warp fills an ST-deep ring of stages, and
-// per-stage mbarriers (full: producer -> consumers, empty: consumers ->
-// producer) order them.  Per stage the producer moves
+// warps only compute, one producer warp fills an ST-deep ring of stages;
+// per stage a full mbarrier (producer -> consumers: every producer lane's
+// cp.async completion plus the TMA bytes) and a named barrier the consumers
+// arrive on without waiting (consumers -> producer, before refill) order
+// them.  Per stage the producer moves
 //   * the filter tile [BM][BC*taps] (row m = w[m0+m][c0..c0+BC)[taps], dense)
 //     with ONE 2-D TMA load straight from the caller's [M][C][hf][wf] tensor
 //     (C*hf*wf*4 bytes per row must be 16-byte aligned; otherwise 4-byte
 //     cp.async per element), out-of-range rows/columns zero-filled;
 //   * the BC-channel halo band with 16-byte / 4-byte cp.async, whose
-//     completion it hands to the stage's full barrier (cp.async.mbarrier.arrive).
+//     completion it hands to the stage's full barrier
+//     (cp.async.mbarrier.arrive.noinc).
 // Padding is written as +0.0 once per tile (it sits at the same positions in
 // every channel and stage), so the producer never stores to shared memory.
 // Consumers read the 16 filters of a (channel, tap) as 16 broadcast scalar
@@ -221,6 +224,7 @@ struct RowWsTile {
   static constexpr int PXN = (RX - 1) * S + WF;
   static constexpr int MIN_BLOCKS = NCW <= 4 ? 2 : 1;
   static_assert(WFLOATS % 32 == 0, "filter tile must keep 128-byte alignment");
+  static_assert(ST >= 1 && ST <= 15, "one named barrier per stage (ids 1..ST)");
 };
 
 template <int HF, int WF, int S, int RX, int WM, int WP, int BC, int ST>
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
   constexpr int RM = T::RM, BM = T::BM, SEG = T::SEG, NCW = T::NCW, TAPS = T::TAPS, WROW = T::WROW;
   constexpr int WFLOATS = T::WFLOATS, PXN = T::PXN;
 
-  // [full[ST] | empty[ST] barriers: 128 B][goff: XCS ints][gtab][pad to 128 B][stages]
+  // [full[ST] barriers: 128 B][goff: XCS ints][gtab][pad to 128 B][stages]
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
   int *goff = reinterpret_cast<int *>(smem_raw + 128);
@@ -259,8 +263,7 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
 
   if (tid == 0) {
     for (int s = 0; s < ST; s++) {
-      mbar_init(smem_u32(&bars[s]), 32);        // producer lanes' cp.async arrivals (+ TMA bytes)
-      mbar_init(smem_u32(&bars[ST + s]), NCW);  // one arrival per consumer warp
+      mbar_init(smem_u32(&bars[s]), 32);        // producer lanes' arrivals (+ TMA bytes)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
       const int s = i % ST;
       const int k = i / ST;
       const uint32_t full = smem_u32(&bars[s]);
-      if (k > 0) mbar_wait(smem_u32(&bars[ST + s]), (k - 1) & 1, p.spin_limit);
+      if (k > 0) named_bar_sync(1 + s, T::NT);  // every consumer is done with the stage's previous chunk
       float *wst = stages + s * stage_floats;
       const int c0 = chunk * BC;
       const int cvalid = min(BC, p.C - c0);
@@ -301,7 +304,7 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
           for (int ct = lane; ct < ctv; ct += 32) cp_async4(wst + m * WROW + ct, wsrc + (long long)m * p.C * TAPS + ct);
       }
       stage_halo_chunk<BC, false>(p, goff, gtab, wst + WFLOATS, xtile + (long long)c0 * hw, cvalid, hw, lane, 32);
-      cp_async_mbar_arrive_noinc(full);
+      cp_async_mbar_arrive_noinc(full);  // the arrive fires when this thread's copies have landed
     }
     if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     return;
@@ -359,8 +362,7 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
       xc += p.XCS;
       wc += TAPS;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(&bars[ST + s]));
+    if (chunk + ST < chunk_end) named_bar_arrive(1 + s, T::NT);  // release the stage for refill
   }
   if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 

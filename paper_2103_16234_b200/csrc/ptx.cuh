@@ -69,6 +69,17 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
+// Named CTA barriers (ids 1..15; 0 is __syncthreads): the consumers of a
+// stage arrive without waiting, the producer that refills it waits.  Used for
+// stage release (write-after-read), where compute-sanitizer's racecheck
+// models the ordering (it does not model an mbarrier ordering later cp.async
+// writes after earlier shared-memory reads).
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 // Raise the transaction count of the current phase without arriving.
 __device__ __forceinline__ void mbar_expect_tx_only(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
