@@ -262,7 +262,7 @@ b2c_status b2c_conv_host(const b2c_conv_desc *d, const float *x_host, const floa
 
 /* A sequence of independent layers (e.g. one inference pass over a network's
  * convolutions) from host buffers: H2D copies, convolutions and D2H copies of
- * consecutive layers overlap on three streams (three device slots, event
+ * consecutive layers overlap on three streams (six device slots, event
  * ordered); synchronous on return.  Pinned host memory gives full PCIe
  * overlap.  engine: B2C_ENGINE_FUSED, _TF32X3 or _TF32.  The batched form of
  * b2c_conv_host for harness loops like the reference's run_bench

@@ -647,7 +647,7 @@ b2c_status b2c_conv_host(const b2c_conv_desc *d, const float *x_host, const floa
 // D2H copies (own stream) of consecutive layers overlap, ordered by events.
 namespace {
 struct Pipeline {
-  static constexpr int kSlots = 3;
+  static constexpr int kSlots = 6;  // in-flight layers: lets the H2D and D2H directions run ahead of each other (layer sizes alternate)
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
   cudaEvent_t loaded[kSlots] = {}, computed[kSlots] = {}, drained[kSlots] = {};
   DeviceBuffers slot[kSlots];

@@ -555,7 +555,8 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
 int device_sm_count(int device) { return sm_count_of(device); }
 
 bool family_has_cluster_epilogue(int fam_id) {
-  return fam_id >= 0 && fam_id < kNumFamilies && !kFamilies[fam_id].strict && kFamilies[fam_id].kind < 3;
+  return fam_id >= 0 && fam_id < kNumFamilies && !kFamilies[fam_id].strict &&
+         (kFamilies[fam_id].kind < 3 || kFamilies[fam_id].kind == 4);
 }
 
 // Measured plans ("find" results of tools/autotune.py, registered at import by
@@ -651,7 +652,9 @@ bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int f
   int r = 0;
   if (out->splits > 1 && !stage1) {
     r = forced_reduce > 0 ? forced_reduce : (tuned_reduce > 0 ? tuned_reduce : (cluster_reduce_enabled() ? 2 : 1));
-    if (r == 2 && (out->splits > 16 || !family_has_cluster_epilogue(out->family))) {
+    // row-segment tiles are contiguous output pixels only when RX divides Wo
+    const bool seg_contig = kFamilies[out->family].kind != 4 || g.Wo % kFamilies[out->family].rx == 0;
+    if (r == 2 && (out->splits > 16 || !family_has_cluster_epilogue(out->family) || !seg_contig)) {
       if (forced_reduce == 2) return false;
       r = 1;
     }

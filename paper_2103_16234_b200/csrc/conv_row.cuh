@@ -307,6 +307,10 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
       cp_async_mbar_arrive_noinc(full);  // the arrive fires when this thread's copies have landed
     }
     if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (!p.cluster) return;
+    // split-C through DSMEM: the producer warp takes part in the tile reduction
+    __syncthreads();  // consumers have parked their accumulators; stages are drained
+    cluster_reduce_tile<BM, SEG * RX, T::NT>(p, stages, m0, s0 * RX);
     return;
   }
 
@@ -366,6 +370,24 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
   }
   if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
+  if (p.cluster) {
+    // split-C through DSMEM (reduce = 2; the planner allows it when RX divides
+    // Wo, so the tile's segments are the contiguous output pixels
+    // [s0*RX, (s0+SEG)*RX)): park the accumulators as a [BM][SEG*RX] tile in
+    // this CTA's (drained) stage memory, then sum the splits' tiles in
+    // ascending rank order — the order stage2_sum_kernel uses, bitwise equal
+    // to partial planes
+    float *tile = stages;
+    const int col = (wp * 32 + lane) * RX;
+    __syncthreads();  // every consumer is past its last stage read (the producer waits here too)
+#pragma unroll
+    for (int r = 0; r < RM; r++)
+#pragma unroll
+      for (int j = 0; j < RX; j++)
+        tile[(wm * RM + r) * (SEG * RX) + col + j] = (r & 1) ? acc[r >> 1][j].y : acc[r >> 1][j].x;
+    cluster_reduce_tile<BM, SEG * RX, T::NT>(p, tile, m0, s0 * RX);
+    return;
+  }
   if (!seg_ok) return;
   float *dst = p.splits > 1 ? p.partials + (long long)split * p.part_stride : p.y;
   const long long pix0 = (long long)n * p.M * p.HoWo + (long long)oy * p.Wo + b * RX;
