@@ -616,7 +616,7 @@ def _e2e_run(lib, nat, cfgs, xs, ws, ys, engine_id, steps, world, device, local_
             "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
             "ms_per_step": round(1e3 * dt / steps, 3),
             "path": "b2c_conv_host_layers (C ABI, pinned host buffers; H2D/compute/D2H of consecutive layers "
-                    "overlapped on 3 streams)"}
+                    "overlapped on 3 streams, 6 device slots)"}
 
 
 TC_TOLERANCE = {"tf32x3": "relative_error vs conv_naive_f64 <= 1e-5*max(1, K/4096) (the fp32 gate)",

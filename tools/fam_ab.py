@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("wl"); ap.add_argument("n", type=int)
 ap.add_argument("--layers", default=""); ap.add_argument("--only", default="")
 ap.add_argument("--splits", default="1")
+ap.add_argument("--reduce", default="0", help="split-C reduction modes to try (0 planner, 1 planes, 2 DSMEM)")
 a = ap.parse_args()
 cfgs = W.layers(a.wl, a.n)
 if a.layers:
@@ -31,9 +32,9 @@ for c in cfgs:
     y = torch.empty(auto.output_shape(), device="cuda")
     res = []
     for fam in matching_families(c):
-        for sp in (int(s) for s in a.splits.split(",")):
+        for sp, red in ((int(s), int(r)) for s in a.splits.split(",") for r in a.reduce.split(",")):
             try:
-                L = ConvLayer(c, family=fam, splits=sp)
+                L = ConvLayer(c, family=fam, splits=sp, reduce=red)
             except Exception:  # noqa: BLE001
                 continue
             if a.only and a.only not in L.family:
