@@ -245,15 +245,21 @@ int max_tile_rows_seg(const Geom &g, int nb, int seg) {
   return worst;
 }
 
-// Row stride of the row-segment kernel's band: >= rc, == W (mod 4) (16-byte
-// staging), and spreading the 32 segment origins of a warp over the 32 banks
-// (scalar pixel loads: one wavefront when all origins differ mod 32).  Scored
-// on the first warps of a sample of tiles.
+// Row stride of the row-segment kernel's band: >= rc, spreading the 32
+// segment origins of a warp over the 32 banks (scalar pixel loads: one
+// wavefront when all origins differ mod 32).  Stride 1: == W (mod 4), so every
+// band row stays 16-byte congruent with its global row (16-byte staging).
+// Stride >= 2: consecutive output rows are S band rows apart, and with RS == W
+// (mod 4) and W % 4 == 0 the origins crowd into a few banks (5-way on ResNet
+// 28->14), so any residue is allowed (rows then stage by 4-byte copies), the
+// congruent one winning ties.  Scored on the first warps of a sample of tiles.
 int pick_row_stride(const Geom &g, int rc, int nb, int rx, int seg) {
   const long long segs = (long long)g.N * g.Ho * nb;
   const long long tiles = cdiv(segs, seg);
-  int best_rs = rc + (((g.W - rc) % 4) + 4) % 4, best_score = INT_MAX;
-  for (int rs = best_rs; rs < best_rs + 64; rs += 4) {
+  const int congruent = rc + (((g.W - rc) % 4) + 4) % 4;
+  const int step = g.S == 1 ? 4 : 1;
+  int best_rs = congruent, best_score = INT_MAX;
+  for (int rs = g.S == 1 ? congruent : rc; rs < congruent + 64; rs += step) {
     int score = 0;
     for (long long t = 0; t < std::min<long long>(tiles, 16); t++) {
       const long long tt = t * std::max<long long>(1, tiles / 16);
@@ -273,6 +279,7 @@ int pick_row_stride(const Geom &g, int rc, int nb, int rx, int seg) {
         score += worst;
       }
     }
+    score = 2 * score + ((rs - congruent) % 4 != 0 ? 1 : 0);  // ties: keep 16-byte staging
     if (score < best_score) {
       best_score = score;
       best_rs = rs;

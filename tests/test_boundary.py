@@ -557,3 +557,59 @@ def test_tc_forced_m_halves():
     p.mode, p.m_halves = 1, 4
     assert lib.b2c_tc_select_tiles(ctypes.byref(nat.desc(cfg)), nat.ENGINE_TF32X3, ctypes.byref(p)) == nat.OK
     assert p.mode == 1
+
+
+def _segment_banks(cfg, t, rx=7):
+    """Banks of the 32 segment origins of each warp of the first tiles of a
+    row-segment plan (the planner's pick_row_stride objective)."""
+    ho, wo = pk.output_dims(cfg)
+    nb = -(-wo // rx)
+    hp = cfg.h + 2 * cfg.pad_h
+    seg = t.bp // rx
+    segs = cfg.n * ho * nb
+    worst = 1
+    for s0 in range(0, min(segs, 8 * seg), seg):
+        r0 = s0 // nb
+        v0 = (r0 // ho) * hp + (r0 % ho) * cfg.stride
+        for w0 in range(s0, min(s0 + seg, segs), 32):
+            banks = {}
+            for sg in range(w0, min(w0 + 32, segs)):
+                r, b = divmod(sg, nb)
+                v = (r // ho) * hp + (r % ho) * cfg.stride
+                bank = ((v - v0) * t.smem_row_stride + b * rx * cfg.stride) % 32
+                banks[bank] = banks.get(bank, 0) + 1
+            worst = max(worst, max(banks.values()))
+    return worst
+
+
+def test_row_segment_plans_layout(native):
+    """Row-segment families (conv_row.cuh): the band row stride keeps every row
+    16-byte congruent with its global row at stride 1 (RS == W mod 4), spreads each warp's
+    32 segment origins over the shared-memory banks (at most 2-way on the
+    BASELINE 3x3 stride-1 layers, 3-way at stride 2), and split-C through DSMEM is offered only when 7
+    divides the output width (the tile is then a contiguous pixel range)."""
+    from paper_2103_16234_b200 import workloads as W
+
+    names = pk.family_names()
+    checked = 0
+    for wl, n in (("c5", 256), ("c4", 8), ("c1", 1)):
+        for cfg in W.layers(wl, n):
+            for f in pk.matching_families(cfg):
+                if "_rws7_" not in names[f] and "_row7_" not in names[f]:
+                    continue
+                t = pk.select_tiles(cfg, family=f, splits=1)
+                if cfg.stride == 1:
+                    assert t.smem_row_stride % 4 == cfg.w % 4, (cfg.name, t.family)
+                assert t.smem_bytes <= 227 * 1024
+                if cfg.hf == 3:  # stride 2: output rows are 2 band rows apart, at best 2-3 way
+                    assert _segment_banks(cfg, t) <= (2 if cfg.stride == 1 else 3), (cfg.name, t.family,
+                                                                                      t.smem_row_stride)
+                checked += 1
+    assert checked > 20
+    odd = pk.ConvConfig("odd", n=2, c=32, h=11, w=11, m=32, hf=3, wf=3, pad_h=1, pad_w=1)  # Wo = 11
+    even = pk.ConvConfig("even", n=2, c=32, h=14, w=14, m=32, hf=3, wf=3, pad_h=1, pad_w=1)  # Wo = 14
+    rws = names.index("fused_3x3s1_rws7_m64")
+    assert pk.select_tiles(even, family=rws, splits=2, reduce=2).reduce == 2
+    with pytest.raises(pk.InvalidPlan):
+        pk.select_tiles(odd, family=rws, splits=2, reduce=2)
+    assert pk.select_tiles(odd, family=rws, splits=2, reduce=1).reduce == 1
