@@ -229,6 +229,10 @@ int max_tile_rows(const Geom &g, int hf_eff, int bp) {
   return worst;
 }
 
+// conv_row_ws_kernel shared layout: [barriers: 128 B][goff: XCS ints][gtab: XCS/4]
+// padded to 128 B, then the stages (also where a DSMEM split-C tile is parked).
+long long ws_tile_offset(int xcs) { return 128 + ((4LL * (xcs + (xcs >> 2)) + 127) & ~127LL); }
+
 // Row-segment kernel: rows of the virtual padded image stack spanned by the
 // worst tile of `seg` segments (nb segments per output row).
 int max_tile_rows_seg(const Geom &g, int nb, int seg) {
@@ -449,7 +453,7 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
       tc.stages = f.stages;
       const long long wfloats = (long long)f.bm * f.bc * taps;
       const long long xfl = ((long long)f.bc * tc.xcs + 31) & ~31LL;
-      smem = 128 + ((4LL * (tc.xcs + (tc.xcs >> 2)) + 127) & ~127LL) + 4LL * f.stages * (wfloats + xfl);
+      smem = ws_tile_offset(tc.xcs) + 4LL * f.stages * (wfloats + xfl);
     }
     if (smem > 226 * 1024) return best.family >= 0 ? (*out = best, true) : false;
     tc.smem_bytes = (int)smem;
@@ -668,7 +672,9 @@ bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int f
   }
   out->reduce = r;
   if (r == 2) {
-    const long long tile_bytes = 4LL * out->bm * out->bp;
+    // the parked tile starts at shared offset 0, except in conv_row_ws_kernel,
+    // which parks it in its stage memory behind the barriers and halo tables
+    const long long tile_bytes = 4LL * out->bm * out->bp + (kFamilies[out->family].kind == 4 ? ws_tile_offset(out->xcs) : 0);
     if (tile_bytes > 226 * 1024) {
       if (forced_reduce == 2) return false;
       out->reduce = 1;
@@ -798,7 +804,7 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   // (at most 16 CTAs; the cluster must fit the GPU)
   int smem = tc.smem_bytes;
   if (!stage1 && !f.strict && tc.splits > 1 && tc.splits <= 16 && tc.reduce == 2) {
-    const int tile_bytes = tc.bm * tc.bp * (int)sizeof(float);
+    const int tile_bytes = tc.bm * tc.bp * (int)sizeof(float) + (f.kind == 4 ? (int)ws_tile_offset(tc.xcs) : 0);
     const int csmem = std::max(smem, tile_bytes);
     const long long key = ((((long long)tc.family * 32 + tc.splits) * 64 + dev) << 18) + csmem;
     int ok = -1;

@@ -304,6 +304,9 @@ CLUSTER_CASES = PLAN_CASES[:5] + [
     pk.ConvConfig("c1x1big", n=2, c=512, h=14, w=14, m=130, hf=1, wf=1),
     pk.ConvConfig("c3big", n=1, c=256, h=28, w=28, m=70, hf=3, wf=3, pad_h=1, pad_w=1),
     pk.ConvConfig("c1x1odd", n=3, c=300, h=7, w=7, m=64, hf=1, wf=1),
+    # row-segment kernels park a [BM][SEG*7] tile behind their halo tables (Wo % 7 == 0)
+    pk.ConvConfig("c3s2", n=2, c=40, h=28, w=28, m=130, hf=3, wf=3, stride=2, pad_h=1, pad_w=1),
+    pk.ConvConfig("c5x5", n=2, c=24, h=14, w=14, m=70, hf=5, wf=5, pad_h=2, pad_w=2),
 ]
 
 

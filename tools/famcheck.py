@@ -8,6 +8,7 @@ from paper_2103_16234_b200 import workloads as W
 
 wl, n, name = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 splits = [int(s) for s in (sys.argv[4] if len(sys.argv) > 4 else "1,2,3").split(",")]
+reduces = [int(s) for s in (sys.argv[5] if len(sys.argv) > 5 else "0").split(",")]
 cfg = next(c for c in W.layers(wl, n) if c.name == name)
 g = torch.Generator(device="cuda").manual_seed(0)
 x = torch.rand((cfg.n, cfg.c, cfg.h, cfg.w), generator=g, device="cuda") * 2 - 1
@@ -15,11 +16,12 @@ w = torch.rand((cfg.m, cfg.c, cfg.hf, cfg.wf), generator=g, device="cuda") * 2 -
 ref = torch.nn.functional.conv2d(x.double(), w.double(), stride=cfg.stride, padding=(cfg.pad_h, cfg.pad_w))
 outs = {}
 for fam in pk.matching_families(cfg):
-    for sp in splits:
+    for sp, red in ((a, b) for a in splits for b in reduces):
         try:
-            L = pk.ConvLayer(cfg, family=fam, splits=sp)
+            L = pk.ConvLayer(cfg, family=fam, splits=sp, reduce=red)
         except Exception:
             continue
+        print("run", L.family, sp, red, flush=True)
         if L.splits != sp:
             continue
         y = L(x, w)
