@@ -28,7 +28,7 @@ TORCH_LIB = PKG / "_b2conv_torch.so"
 TORCH_SRC = CSRC / "torch_ext.cpp"
 SOURCES = [CSRC / "conv_launch.cu", CSRC / "conv_tc.cu", CSRC / "probe.cu", CSRC / "api.cpp"]
 DEPS = SOURCES + [CSRC / "conv_kernel.cuh", CSRC / "conv1x1_vec.cuh", CSRC / "conv_tc.cuh", CSRC / "conv_row.cuh",
-                  CSRC / "conv1x1_ws.cuh", CSRC / "ptx.cuh", CSRC / "internal.h", ROOT / "include" / "b2conv.h"]
+                  CSRC / "conv1x1_ws.cuh", CSRC / "conv1x1_tma.cuh", CSRC / "ptx.cuh", CSRC / "internal.h", ROOT / "include" / "b2conv.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # No --use_fast_math / -ftz: denormals and IEEE rounding must match numpy.

@@ -426,7 +426,7 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
   if (!ws_ok && forced_splits > 1)
     return fail(B2C_INVALID_ARGUMENT, "split %d needs a %lld-byte workspace, %lld provided", forced_splits,
                 (long long)tc.ws_bytes, (long long)workspace_size);
-  const bool needs_align = tc.kind == 1;
+  const bool needs_align = tc.kind == 1 || tc.kind == 6;
   if (needs_align && !aligned && forced >= 0)
     return fail(B2C_INVALID_ARGUMENT, "family %s needs 16-byte aligned x, w, y and workspace", b2c::family_name(forced));
   if (!ws_ok || (needs_align && !aligned)) {

@@ -22,6 +22,7 @@
 
 #include "conv1x1_vec.cuh"
 #include "conv1x1_ws.cuh"
+#include "conv1x1_tma.cuh"
 #include "conv_kernel.cuh"
 #include "conv_row.cuh"
 #include "internal.h"
@@ -41,7 +42,8 @@ struct Family {
   int kind;             // 0: conv_direct_kernel (halo staging), 1: conv1x1_vec_kernel, 2: its 4-byte variant,
                         // 3: conv_row_kernel (row segments, halo staging), 4: its warp-specialised
                         //    variant (producer warp, mbarrier ring, TMA filter tiles), 5: the
-                        //    warp-specialised pointwise kernel (conv1x1_ws.cuh, any stride)
+                        //    warp-specialised pointwise kernel (conv1x1_ws.cuh, any stride), 6: the
+                        //    TMA-fed pointwise kernel (conv1x1_tma.cuh)
   int stages;           // cp.async pipeline depth of kind 1
   int tm = 2;           // pointwise kernels: channel groups of 4 per thread (4: 16 channels x 8 pixels)
   int rx = 0;           // kind 3: outputs per row segment
@@ -109,6 +111,14 @@ struct Family {
     NAME, 1, 1, 1, Pw1x1WsTile<WM, WP, BC, ST>::BM, Pw1x1WsTile<WM, WP, BC, ST>::BP, BC, false,            \
         Pw1x1WsTile<WM, WP, BC, ST>::NT, reinterpret_cast<const void *>(&conv1x1_ws_kernel<WM, WP, BC, ST>), \
         Pw1x1WsTile<WM, WP, BC, ST>::MIN_BLOCKS, 5, ST, 4                                                   \
+  }
+
+// TMA-fed pointwise kernel (kind 6)
+#define B2C_PW1X1TMA(NAME, WM, WP, BC, ST)                                                                  \
+  Family {                                                                                                 \
+    NAME, 1, 1, 1, Pw1x1TmaTile<WM, WP, BC, ST>::BM, Pw1x1TmaTile<WM, WP, BC, ST>::BP, BC, false,          \
+        Pw1x1TmaTile<WM, WP, BC, ST>::NT, reinterpret_cast<const void *>(&conv1x1_tma_kernel<WM, WP, BC, ST>), \
+        Pw1x1TmaTile<WM, WP, BC, ST>::MIN_BLOCKS, 6, ST, 2                                                  \
   }
 
 const Family kFamilies[] = {
@@ -195,6 +205,10 @@ const Family kFamilies[] = {
     // persistent warp-specialised pointwise families (conv1x1_ws.cuh)
     B2C_PW1X1WS("fused_1x1ws_m64", 4, 2, 16, 4),
     B2C_PW1X1WS("fused_1x1ws_m128", 8, 1, 16, 4),
+    // TMA-fed pointwise families (conv1x1_tma.cuh)
+    B2C_PW1X1TMA("fused_1x1t_m64", 2, 4, 16, 3),
+    B2C_PW1X1TMA("fused_1x1t_m128", 4, 2, 16, 3),
+    B2C_PW1X1TMA("fused_1x1t_m64p128", 2, 2, 16, 3),
 };
 constexpr int kNumFamilies = sizeof(kFamilies) / sizeof(kFamilies[0]);
 
@@ -314,6 +328,7 @@ double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, in
   // persistent pointwise: measured on par with the 16-byte pointwise families on
   // stride-1 planes, ahead on strided / 4-byte-staged ones (profiles/ab/r2_pointwise_ws_ab.txt)
   if (tc.kind == 5) lds_penalty = (g.S == 1 && (long long)g.H * g.W % 4 == 0) ? 1.15 : 0.9;
+  if (tc.kind == 6) lds_penalty = 0.95;  // no per-thread staging, no CTA-wide barrier
   const double fma = (double)tc.bm * tc.bp * taps * tc.bc * tc.chunks_per_split * (stage1 ? 2.0 : 1.0) * lds_penalty;
   const double per_elem = (tc.kind == 1 || (tc.kind == 5 && g.S == 1 && (long long)g.H * g.W % 4 == 0) || ((long long)g.H * g.W % 4 == 0 && (tc.kind == 0 || tc.kind >= 3))) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
   const double loads = (per_elem * tc.tile_elems + 4.0 * tc.bm * taps) * tc.bc * tc.chunks_per_split;
@@ -353,7 +368,7 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
   base.bc = f.bc;
   base.threads = f.threads;
   base.kind = f.kind;
-  if (f.kind == 1 || f.kind == 2 || f.kind == 5) {
+  if (f.kind == 1 || f.kind == 2 || f.kind == 5 || f.kind == 6) {
     base.rs = g.W;
     base.rows = 1;
     base.tile_elems = f.bp;
@@ -383,13 +398,15 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
       if (f.kind == 2) smem = std::max(smem, 4LL * f.bm * f.bp);  // epilogue transposes the tile in smem
       if (f.kind == 5)  // barriers | ST x (filter tile | pixel tile)
         smem = 128 + 4LL * f.stages * ((long long)f.bm * f.bc + (long long)f.bc * f.bp);
+      if (f.kind == 6)  // barriers | ST x (filter tile [BM][BC+4] | two pixel boxes [BC][BP])
+        smem = 128 + 4LL * f.stages * ((long long)f.bm * (f.bc + 4) + 2LL * f.bc * f.bp);
       if (smem > 226 * 1024) return false;
       tc.smem_bytes = (int)smem;
       const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
       tc.occupancy = std::max(1, std::min({f.max_ctas_per_sm, by_smem, 2048 / f.threads}));
       tc.ws_bytes = tc.splits > 1 ? 4LL * tc.splits * g.N * g.M * g.HoWo : 0;
       tc.cost = model_cost(g, tc, 1, false, sms, tc.occupancy) * (f.kind == 1 && f.tm == 2 ? 1.12 : 1.0);
-      if (f.kind == 5) tc.stages = f.stages;
+      if (f.kind >= 5) tc.stages = f.stages;
       if (tc.cost < best.cost) {
         best.family = fam_id;
         best.tc = tc;
@@ -556,6 +573,9 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
   if (stage1) return g.S == 1;
   if (f.kind == 3 || f.kind == 4)
     return f.hf == g.HF && f.wf == g.WF && f.s == g.S && (long long)g.N * g.Ho * g.Wo < (1LL << 30);
+  if (f.kind == 6)  // TMA boxes: 16-byte global strides, a tile spans at most two images
+    return g.HF == 1 && g.WF == 1 && g.S == 1 && g.PH == 0 && g.PW == 0 && ((long long)g.H * g.W) % 4 == 0 &&
+           g.C % 4 == 0 && g.HoWo >= f.bp && g.N < (1 << 30);
   if (f.kind == 5)  // gather offsets relative to a tile's first image stay in int32
     return g.HF == 1 && g.WF == 1 && g.PH == 0 && g.PW == 0 &&
            (cdiv(f.bp, g.HoWo) + 2) * (long long)g.C * g.H * g.W < INT_MAX;
@@ -615,7 +635,7 @@ bool plan_tiles_core(const Geom &g, bool stage1, int device, int forced_family, 
       auto it = g_tuned.find(tuned_key(g, stage1));
       if (it != g_tuned.end()) t = it->second;
     }
-    if (t.family >= 0 && (allow_split || t.splits <= 1) && (allow_vec || kFamilies[t.family].kind != 1) &&
+    if (t.family >= 0 && (allow_split || t.splits <= 1) && (allow_vec || (kFamilies[t.family].kind != 1 && kFamilies[t.family].kind != 6)) &&
         (!need_cluster || family_has_cluster_epilogue(t.family)) &&
         family_matches(t.family, g, stage1) &&
         evaluate(g, t.family, stage1, sms, t.splits, allow_split, &best)) {
@@ -634,7 +654,7 @@ bool plan_tiles_core(const Geom &g, bool stage1, int device, int forced_family, 
     for (int i = 0; i < kNumFamilies; i++) {
       const Family &f = kFamilies[i];
       if (!family_matches(i, g, stage1)) continue;
-      if (!allow_vec && f.kind == 1) continue;
+      if (!allow_vec && (f.kind == 1 || f.kind == 6)) continue;  // need 16-byte aligned operands
       if (need_cluster && !family_has_cluster_epilogue(i)) continue;
       const bool generic = (f.hf == 0) && !stage1;
       if ((pass == 0) == generic) continue;  // specialised families first
@@ -685,15 +705,13 @@ bool plan_tiles(const Geom &g, bool stage1, int device, int forced_family, int f
   return true;
 }
 
-// 2-D tensor map of the filter bank viewed as [M][C*hf*wf] (row-major, fp32)
-// for conv_row_ws_kernel's per-stage TMA tile {BC*hf*wf, BM}.  false when TMA
-// cannot address it (row pitch not a multiple of 16 bytes, unaligned base, a
-// box dimension above 256): the kernel then stages filters by cp.async.
-bool encode_filter_map(CUtensorMap *map, const Geom &g, const float *w, int bm, int bc) {
-  using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static EncodeFn encode = [] {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda),
+// resolved once; nullptr if the driver lacks it.
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn tensor_map_encoder() {
+  static const EncodeFn encode = [] {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
@@ -702,8 +720,17 @@ bool encode_filter_map(CUtensorMap *map, const Geom &g, const float *w, int bm, 
     cudaGetLastError();
     return reinterpret_cast<EncodeFn>(fn);
   }();
+  return encode;
+}
+
+// 2-D tensor map of the filter bank viewed as [M][C*hf*wf] (row-major, fp32)
+// for conv_row_ws_kernel's per-stage TMA tile {BC*hf*wf, BM}.  false when TMA
+// cannot address it (row pitch not a multiple of 16 bytes, unaligned base, a
+// box dimension above 256): the kernel then stages filters by cp.async.
+bool encode_filter_map(CUtensorMap *map, const Geom &g, const float *w, int bm, int bc, int extra_cols = 0) {
+  const EncodeFn encode = tensor_map_encoder();
   const long long row = (long long)g.C * g.HF * g.WF;
-  const int box0 = bc * g.HF * g.WF;
+  const int box0 = bc * g.HF * g.WF + extra_cols;
   if (!encode || (row * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(w) & 15) != 0 || box0 > 256 || bm > 256 ||
       (box0 * 4) % 16 != 0)
     return false;
@@ -712,6 +739,22 @@ bool encode_filter_map(CUtensorMap *map, const Geom &g, const float *w, int bm, 
   const cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)bm};
   const cuuint32_t estr[2] = {1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(w), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 3-D tensor map of the input viewed as [N][C][H*W] for conv1x1_tma_kernel's
+// pixel boxes {BP, BC, 1} (out-of-range pixels and channels zero-filled).
+bool encode_input_map(CUtensorMap *map, const Geom &g, const float *x, int bp, int bc) {
+  const EncodeFn encode = tensor_map_encoder();
+  const long long hw = (long long)g.H * g.W;
+  if (!encode || (hw * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0 || bp > 256 || bc > 256)
+    return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)hw, (cuuint64_t)g.C, (cuuint64_t)g.N};
+  const cuuint64_t strides[2] = {(cuuint64_t)(hw * 4), (cuuint64_t)(hw * 4 * g.C)};
+  const cuuint32_t box[3] = {(cuuint32_t)bp, (cuuint32_t)bc, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(x), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -762,6 +805,10 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   CUtensorMap wmap;
   std::memset(&wmap, 0, sizeof(wmap));
   if (f.kind == 4 || f.kind == 5) p.w_tma = encode_filter_map(&wmap, g, w, tc.bm, tc.bc) ? 1 : 0;
+  CUtensorMap xmap;
+  std::memset(&xmap, 0, sizeof(xmap));
+  if (f.kind == 6 && !(encode_filter_map(&wmap, g, w, tc.bm, tc.bc, 4) && encode_input_map(&xmap, g, x, tc.bp, tc.bc)))
+    return cudaErrorNotSupported;  // the planner only offers kind 6 where both maps encode
   p.spin_limit = watchdog_ns();
   if (f.kind == 3 || f.kind == 4) {
     p.nb = (int)cdiv(g.Wo, f.rx);
@@ -857,7 +904,7 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
     const long long slots = (long long)sm_count_of(dev) * resident_ctas(tc.family, f.kernel, tc.threads, smem, dev);
     grid = dim3((unsigned)std::max<long long>(1, std::min(items, slots)), 1, 1);
   }
-  void *args[] = {&p, &wmap};  // the second is read by kind 4 only
+  void *args[] = {&p, &wmap, &xmap};  // the maps are read by kinds 4-6 only
   note_launch();
   cudaError_t err;
   if (p.pdl || p.cluster) {
