@@ -183,6 +183,8 @@ PLAN_CASES = [
     pk.ConvConfig("ps2", n=2, c=24, h=15, w=15, m=20, hf=3, wf=3, stride=2, pad_h=1, pad_w=1),
     pk.ConvConfig("p7", n=2, c=3, h=30, w=30, m=20, hf=7, wf=7, stride=2, pad_h=3, pad_w=3),
     pk.ConvConfig("pe", n=2, c=9, h=9, w=10, m=17, hf=2, wf=4, pad_h=1, pad_w=2),
+    # pointwise with H*W % 4 == 0: 16-byte, persistent and TMA-fed families (tiles across images)
+    pk.ConvConfig("p1v", n=3, c=72, h=16, w=16, m=100, hf=1, wf=1),
 ]
 
 

@@ -19,6 +19,7 @@ import paper_2103_16234_b200 as pk  # noqa: E402
 CASES = [
     pk.ConvConfig("3x3", n=2, c=24, h=14, w=14, m=40, hf=3, wf=3, pad_h=1, pad_w=1),
     pk.ConvConfig("1x1v", n=2, c=64, h=14, w=14, m=48, hf=1, wf=1),
+    pk.ConvConfig("1x1t", n=3, c=48, h=16, w=16, m=72, hf=1, wf=1),
     pk.ConvConfig("1x1odd", n=3, c=40, h=7, w=7, m=36, hf=1, wf=1),
     pk.ConvConfig("1x1s2", n=2, c=32, h=14, w=14, m=40, hf=1, wf=1, stride=2),
     pk.ConvConfig("5x5", n=1, c=16, h=14, w=14, m=32, hf=5, wf=5, pad_h=2, pad_w=2),
@@ -41,7 +42,7 @@ def main():
         fams = pk.matching_families(cfg)
         if quick:  # two round-1 families plus every row-segment / warp-specialised one
             names = pk.family_names()
-            fams = fams[:2] + [f for f in fams[2:] if any(k in names[f] for k in ("row7", "rws7", "1x1ws"))]
+            fams = fams[:2] + [f for f in fams[2:] if any(k in names[f] for k in ("row7", "rws7", "1x1ws", "1x1t_"))]
         for fam in fams:
             for splits, reduce in ((1, 0), (2, 1), (2, 2)):
                 try:
