@@ -224,7 +224,7 @@ struct RowWsTile {
   static constexpr int PXN = (RX - 1) * S + WF;
   static constexpr int MIN_BLOCKS = NCW <= 4 ? 2 : 1;
   static_assert(WFLOATS % 32 == 0, "filter tile must keep 128-byte alignment");
-  static_assert(ST >= 1 && ST <= 15, "one named barrier per stage (ids 1..ST)");
+  static_assert(ST >= 1 && ST <= 14, "one named barrier per stage (ids 1..ST; 15: cluster epilogue)");
 };
 
 template <int HF, int WF, int S, int RX, int WM, int WP, int BC, int ST>
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
     if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (!p.cluster) return;
     // split-C through DSMEM: the producer warp takes part in the tile reduction
-    __syncthreads();  // consumers have parked their accumulators; stages are drained
+    // (its first cluster barrier orders it after the consumers' tile writes)
     cluster_reduce_tile<BM, SEG * RX, T::NT>(p, stages, m0, s0 * RX);
     return;
   }
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
     // to partial planes
     float *tile = stages;
     const int col = (wp * 32 + lane) * RX;
-    __syncthreads();  // every consumer is past its last stage read (the producer waits here too)
+    named_bar_sync(15, NCW * 32);  // every consumer is past its last stage read before the tile overlays them
 #pragma unroll
     for (int r = 0; r < RM; r++)
 #pragma unroll
