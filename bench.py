@@ -297,24 +297,38 @@ def make_operands(cfgs, device, seed):
     return xs, ws, ys
 
 
-def time_layers(layers, xs, ws, ys, reps=20):
-    """Per-layer mean kernel time (ms), each layer replayed back to back
-    (L2-warm, isolated) -- used only by the --report sweep."""
+def graph_time(fn, reps):
+    """Device time (ms) of one call of ``fn``: ``reps`` calls captured in a CUDA
+    graph, the graph replayed 3 times (median) -- host launch overhead (Python,
+    ctypes, planning) stays out, so small layers show their kernel time."""
     import torch
 
-    out = []
-    stream = torch.cuda.current_stream()
-    for L, x, w, y in zip(layers, xs, ws, ys):
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
         for _ in range(3):
-            L(x, w, out=y)
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(3):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(reps):
-            L(x, w, out=y)
-        b.record(stream)
+        a.record()
+        g.replay()
+        b.record()
         b.synchronize()
-        out.append(a.elapsed_time(b) / reps)
-    return out
+        ts.append(a.elapsed_time(b) / reps)
+    return sorted(ts)[1]
+
+
+def time_layers(layers, xs, ws, ys, reps=20):
+    """Per-layer kernel time (ms), each layer replayed back to back in a CUDA
+    graph (L2-warm, isolated) -- used only by the --report sweep."""
+    return [graph_time(lambda L=L, x=x, w=w, y=y: L(x, w, out=y), reps) for L, x, w, y in zip(layers, xs, ws, ys)]
 
 
 def time_layers_in_step(layers, xs, ws, ys, passes=3):
@@ -416,17 +430,12 @@ def time_cudnn(cfgs, xs, ws, reps=10):
     torch.backends.cudnn.benchmark = True
     out = []
     for c, x, w in zip(cfgs, xs, ws):
-        def run():
+        def run(c=c, x=x, w=w):
             return F.conv2d(x, w, stride=c.stride, padding=(c.pad_h, c.pad_w))
-        for _ in range(3):
+        for _ in range(3):  # benchmark-mode algorithm selection before capture
             run()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(reps):
-            run()
-        b.record()
-        b.synchronize()
-        out.append(a.elapsed_time(b) / reps)
+        torch.cuda.synchronize()
+        out.append(graph_time(run, reps))
     torch.backends.cudnn.benchmark = False
     return out
 
