@@ -202,6 +202,9 @@ const Family kFamilies[] = {
     // single-chunk layers (ResNet conv1, C = 3): one stage, two CTAs per SM
     B2C_ROWWS("fused_7x7s2_rws7_m64st1", 7, 7, 2, 7, 4, 1, 4, 1),
     B2C_ROWWS("fused_7x7s2_rws7_m32st1", 7, 7, 2, 7, 2, 2, 4, 1),
+    // 3-channel stages (ResNet conv1): the filter rows of a tile are one contiguous bulk copy
+    B2C_ROWWS("fused_7x7s2_rws7_m64c3", 7, 7, 2, 7, 4, 1, 3, 1),
+    B2C_ROWWS("fused_7x7s2_rws7_m32c3", 7, 7, 2, 7, 2, 2, 3, 1),
     // persistent warp-specialised pointwise families (conv1x1_ws.cuh)
     B2C_PW1X1WS("fused_1x1ws_m64", 4, 2, 16, 4),
     B2C_PW1X1WS("fused_1x1ws_m128", 8, 1, 16, 4),
@@ -805,6 +808,14 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   CUtensorMap wmap;
   std::memset(&wmap, 0, sizeof(wmap));
   if (f.kind == 4 || f.kind == 5) p.w_tma = encode_filter_map(&wmap, g, w, tc.bm, tc.bc) ? 1 : 0;
+  if (f.kind == 4 && g.C == tc.bc) {
+    // one chunk holding every channel: each tile's filter rows are one contiguous
+    // block, moved by a single bulk copy when 16-byte sized and aligned (conv1: C = 3)
+    const long long row_bytes = 4LL * g.C * g.HF * g.WF;
+    const bool aligned = (reinterpret_cast<uintptr_t>(w) & 15) == 0 && (tc.bm * row_bytes) % 16 == 0 &&
+                         (g.M % tc.bm == 0 || ((g.M % tc.bm) * row_bytes) % 16 == 0);
+    if (aligned) p.w_tma = 2;
+  }
   CUtensorMap xmap;
   std::memset(&xmap, 0, sizeof(xmap));
   if (f.kind == 6 && !(encode_filter_map(&wmap, g, w, tc.bm, tc.bc, 4) && encode_input_map(&xmap, g, x, tc.bp, tc.bc)))

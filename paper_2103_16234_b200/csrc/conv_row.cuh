@@ -292,7 +292,15 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
       float *wst = stages + s * stage_floats;
       const int c0 = chunk * BC;
       const int cvalid = min(BC, p.C - c0);
-      if (tma) {
+      if (p.w_tma == 2) {
+        // the family's chunk is all C channels (BC == C): the tile's filter rows
+        // are one contiguous block of the caller's tensor -> one bulk copy
+        if (lane == 0) {
+          const uint32_t bytes = 4u * (uint32_t)min(BM, p.M - m0) * WROW;
+          mbar_expect_tx_only(full, bytes);
+          bulk_copy_g2s(smem_u32(wst), p.w + (long long)m0 * WROW, bytes, full);
+        }
+      } else if (tma) {
         if (lane == 0) {
           mbar_expect_tx_only(full, WFLOATS * 4);
           tma_load_2d(smem_u32(wst), &wmap, c0 * TAPS, m0, full);
