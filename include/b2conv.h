@@ -25,12 +25,13 @@
  *  - Determinism: every engine is deterministic run to run
  *    (no atomics on data).  Each output's summation order is a function of
  *    (c, hf, wf) for the paper-faithful two-stage engine — bitwise
- *    independent of any plan — of (c, hf, wf, splits) for the fused engine
- *    (independent of the kernel family and of the split-C reduction mode),
- *    and of (mode, splits) for the tensor-core engines.  Images are
- *    independent, so a batch sharded across GPUs is bitwise identical to the
- *    unsharded result when each shard runs the global plan's splits
- *    (sharding.shard_layer pins them).
+ *    independent of any plan — of (c, hf, wf) and the split-C channel ranges
+ *    for the fused engine (ranges = split count x the family's channels per
+ *    pipeline chunk; otherwise independent of the kernel family and of the
+ *    split-C reduction mode), and of (mode, splits) for the tensor-core
+ *    engines.  Images are independent, so a batch sharded across GPUs is
+ *    bitwise identical to the unsharded result when each shard keeps the
+ *    global plan's channel ranges (sharding.shard_layer pins them).
  */
 #ifndef B2CONV_H
 #define B2CONV_H
