@@ -185,6 +185,8 @@ PLAN_CASES = [
     pk.ConvConfig("pe", n=2, c=9, h=9, w=10, m=17, hf=2, wf=4, pad_h=1, pad_w=2),
     # pointwise with H*W % 4 == 0: 16-byte, persistent and TMA-fed families (tiles across images)
     pk.ConvConfig("p1v", n=3, c=72, h=16, w=16, m=100, hf=1, wf=1),
+    # pointwise on 7x7 planes with C % 4 == 0: whole-image tiles by bulk copy (partial last tile)
+    pk.ConvConfig("p1img", n=7, c=48, h=7, w=7, m=80, hf=1, wf=1),
 ]
 
 

@@ -20,6 +20,7 @@ CASES = [
     pk.ConvConfig("3x3", n=2, c=24, h=14, w=14, m=40, hf=3, wf=3, pad_h=1, pad_w=1),
     pk.ConvConfig("1x1v", n=2, c=64, h=14, w=14, m=48, hf=1, wf=1),
     pk.ConvConfig("1x1t", n=3, c=48, h=16, w=16, m=72, hf=1, wf=1),
+    pk.ConvConfig("1x1img", n=7, c=48, h=7, w=7, m=80, hf=1, wf=1),
     pk.ConvConfig("1x1odd", n=3, c=40, h=7, w=7, m=36, hf=1, wf=1),
     pk.ConvConfig("1x1s2", n=2, c=32, h=14, w=14, m=40, hf=1, wf=1, stride=2),
     pk.ConvConfig("5x5", n=1, c=16, h=14, w=14, m=32, hf=5, wf=5, pad_h=2, pad_w=2),
