@@ -422,11 +422,11 @@ b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const floa
   if (st != B2C_OK) return st;
   const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
                          reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(workspace)) & 15) == 0;
-  const bool ws_ok = tc.splits <= 1 || (workspace && workspace_size >= tc.ws_bytes);
-  if (!ws_ok && forced_splits > 1)
-    return fail(B2C_INVALID_ARGUMENT, "split %d needs a %lld-byte workspace, %lld provided", forced_splits,
-                (long long)tc.ws_bytes, (long long)workspace_size);
-  const bool needs_align = tc.kind == 1 || tc.kind == 6;
+  const bool ws_ok = tc.ws_bytes == 0 || (workspace && workspace_size >= tc.ws_bytes);
+  if (!ws_ok && (forced_splits > 1 || (forced >= 0 && tc.kind == 9)))
+    return fail(B2C_INVALID_ARGUMENT, "plan %s split %d needs a %lld-byte workspace, %lld provided",
+                b2c::family_name(tc.family), tc.splits, (long long)tc.ws_bytes, (long long)workspace_size);
+  const bool needs_align = tc.kind == 1 || tc.kind == 6 || tc.kind == 9;
   if (needs_align && !aligned && forced >= 0)
     return fail(B2C_INVALID_ARGUMENT, "family %s needs 16-byte aligned x, w, y and workspace", b2c::family_name(forced));
   if (!ws_ok || (needs_align && !aligned)) {

@@ -94,9 +94,17 @@ __device__ __forceinline__ void vec_cluster_epilogue(const KParams &p, const flo
 // chunks per tile).  Per-item setup is a few integer ops per thread: every
 // thread's pixel group is the same for all of its channel rows, and its filter
 // elements are fixed (m, c) offsets.
-template <int WM, int WP, int BC, bool VEC = true, int TM = 2>
+//
+// PACKED (kind 9, with VEC): p.x is not the caller's x but its pixels packed by
+// pack_pixels_kernel into x'[C][qp] (q = n*Ho*Wo + oy*Wo + ox, the stride
+// applied), so 4 consecutive pixels are one 16-byte group whatever the plane
+// size or stride — the 16-byte path for 7x7 planes and projection shortcuts.
+// Outputs are stored to the caller's NCHW y (float4 when Ho*Wo % 4 == 0, else
+// per pixel).  Same per-output arithmetic as every other pointwise family.
+template <int WM, int WP, int BC, bool VEC = true, int TM = 2, bool PACKED = false>
 __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC, TM>::NT, Vec1x1Tile<WM, WP, BC, TM>::MIN_BLOCKS)
     conv1x1_vec_kernel(const KParams p) {
+  static_assert(!PACKED || VEC, "packed pixels are staged as 16-byte groups");
   using T = Vec1x1Tile<WM, WP, BC, TM>;
   constexpr int BM = T::BM, BP = T::BP, NT = T::NT, WS = T::WS, STAGES = T::STAGES;
   constexpr int GPR = BP / 4;                  // 16-byte pixel groups per channel row of a chunk
@@ -112,7 +120,7 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC, TM>::NT, Vec1x1Tile<WM,
   const int wm = wid / WP, wp = wid - (wid / WP) * WP;
   const int mgi = lane >> 3, pgi = lane & 7;
   const int hw = p.HoWo;            // output plane (== input plane for VEC: 1x1, stride 1, no padding)
-  const int in_hw = p.H * p.W;      // input plane (!VEC may subsample: stride S, no padding)
+  const int in_hw = PACKED ? p.qp : p.H * p.W;  // input plane (!VEC may subsample: stride S, no padding)
   const long long chw = (long long)p.C * in_hw;
   const long long tiles = (long long)p.mtiles * p.ptiles;
   const long long items = tiles * p.splits;
@@ -153,7 +161,9 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC, TM>::NT, Vec1x1Tile<WM,
       if (q < p.Q) {
         const int n = q / hw;
         const int r = q - n * hw;
-        if (VEC) {
+        if (PACKED) {
+          xoff[e] = (Off)q;
+        } else if (VEC) {
           xoff[e] = (Off)((long long)n * chw + r);
         } else {
           const int oy = r / p.Wo;
@@ -305,6 +315,24 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC, TM>::NT, Vec1x1Tile<WM,
       store_tile_coalesced<BM, BP, NT>(p, smem, dst, m0, q0, 0, BM * BP);
       break;
     }
+    if (PACKED && !p.vec_out) {  // Ho*Wo % 4 != 0: a 4-pixel group may straddle two images
+#pragma unroll
+      for (int g = 0; g < 2; g++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const int q = q0 + xcol + 32 * g + j;
+          if (q >= p.Q) continue;
+          const int n = q / hw;
+          const long long base = (long long)n * p.M * hw + (q - n * hw);
+#pragma unroll
+          for (int r = 0; r < 4 * TM; r++) {
+            const int m = m0 + wrow_s + (r & 3) + (r >> 2) * 16;
+            if (m >= p.M) continue;
+            const float2 a = acc[r >> 1][4 * g + j];
+            dst[base + (long long)m * hw] = (r & 1) ? a.y : a.x;
+          }
+        }
+    } else
 #pragma unroll
     for (int g = 0; g < 2; g++) {
       const int q = q0 + xcol + 32 * g;
@@ -338,6 +366,33 @@ __global__ void __launch_bounds__(Vec1x1Tile<WM, WP, BC, TM>::NT, Vec1x1Tile<WM,
     const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     p.trace[5 * cta + 4] = global_ns();
   }
+}
+
+// Pixel packing for the packed pointwise families (kind 9): xp[c][q] =
+// x[n][c][oy*S][ox*S] for q = n*Ho*Wo + oy*Wo + ox < Q, +0.0 for Q <= q < qp.
+// HBM-bound gather (grid: qp/4/256 x C); its output stays largely in L2 for the
+// convolution that follows.
+__global__ void __launch_bounds__(256) pack_pixels_kernel(const KParams p, const float *__restrict__ x,
+                                                          float *__restrict__ xp) {
+  const int c = blockIdx.y;
+  const int q = 4 * (blockIdx.x * 256 + threadIdx.x);
+  if (q >= p.qp) return;
+  const long long chw = (long long)p.C * p.H * p.W;
+  const float *xc = x + (long long)c * p.H * p.W;
+  float v[4];
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const int qq = q + j;
+    v[j] = 0.0f;
+    if (qq < p.Q) {
+      const int n = fdiv(qq, p.mHoWo);
+      const int r = qq - n * p.HoWo;
+      const int oy = fdiv(r, p.mWo);
+      const int ox = r - oy * p.Wo;
+      v[j] = __ldg(xc + n * chw + (long long)oy * p.S * p.W + ox * p.S);
+    }
+  }
+  *reinterpret_cast<float4 *>(xp + (long long)c * p.qp + q) = make_float4(v[0], v[1], v[2], v[3]);
 }
 
 }  // namespace b2c

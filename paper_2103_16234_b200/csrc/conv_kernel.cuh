@@ -77,6 +77,7 @@ struct KParams {
   int segs;                   // row-segment kernel: N*Ho*nb segments
   int w_tma;                  // warp-specialised row kernel: filter tiles by 2-D TMA (tensor map argument)
   unsigned long long spin_limit;  // mbarrier wait bound (ns) before __trap; 0 = unbounded (watchdog_ns())
+  int qp;                     // packed pointwise (kind 9): row pitch of the packed pixels x'[C][qp], qp = Q rounded up to 4
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {

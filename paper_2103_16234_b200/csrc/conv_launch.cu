@@ -43,7 +43,8 @@ struct Family {
                         // 3: conv_row_kernel (row segments, halo staging), 4: its warp-specialised
                         //    variant (producer warp, mbarrier ring, TMA filter tiles), 5: the
                         //    warp-specialised pointwise kernel (conv1x1_ws.cuh, any stride), 6: the
-                        //    TMA-fed pointwise kernel (conv1x1_tma.cuh)
+                        //    TMA-fed pointwise kernel (conv1x1_tma.cuh), 9: conv1x1_vec_kernel on
+                        //    packed pixels (pack_pixels_kernel first)
   int stages;           // cp.async pipeline depth of kind 1
   int tm = 2;           // pointwise kernels: channel groups of 4 per thread (4: 16 channels x 8 pixels)
   int rx = 0;           // kind 3: outputs per row segment
@@ -77,6 +78,14 @@ struct Family {
         Vec1x1Tile<WM, WP, BC, 4>::NT,                                                                     \
         reinterpret_cast<const void *>(&conv1x1_vec_kernel<WM, WP, BC, true, 4>),                          \
         Vec1x1Tile<WM, WP, BC, 4>::MIN_BLOCKS, 1, Vec1x1Tile<WM, WP, BC, 4>::STAGES, 4                     \
+  }
+// packed-pixel variants (kind 9): pack_pixels_kernel, then the 16-byte kernel on x'[C][qp]
+#define B2C_PK1X1(NAME, WM, WP, BC, TM)                                                                    \
+  Family {                                                                                                 \
+    NAME, 1, 1, 1, Vec1x1Tile<WM, WP, BC, TM>::BM, Vec1x1Tile<WM, WP, BC, TM>::BP, BC, false,              \
+        Vec1x1Tile<WM, WP, BC, TM>::NT,                                                                    \
+        reinterpret_cast<const void *>(&conv1x1_vec_kernel<WM, WP, BC, true, TM, true>),                    \
+        Vec1x1Tile<WM, WP, BC, TM>::MIN_BLOCKS, 9, Vec1x1Tile<WM, WP, BC, TM>::STAGES, TM                  \
   }
 // 4-byte staging variant for planes with H*W % 4 != 0 (kind 2)
 #define B2C_SCA1X1(NAME, WM, WP, BC)                                                                       \
@@ -168,6 +177,12 @@ const Family kFamilies[] = {
     B2C_VEC1X1W("fused_1x1w_m128", 2, 2, 16),
     B2C_VEC1X1W("fused_1x1w_m256", 4, 1, 16),
     B2C_VEC1X1W("fused_1x1w_m128p256", 2, 4, 16),
+    // pointwise on packed pixels (7x7 planes, strided projection shortcuts)
+    B2C_PK1X1("fused_1x1pk_m64", 2, 4, 16, 2),
+    B2C_PK1X1("fused_1x1pk_m64b32", 2, 4, 32, 2),
+    B2C_PK1X1("fused_1x1pk_m128", 4, 2, 16, 2),
+    B2C_PK1X1("fused_1x1pkw_m64", 1, 4, 16, 4),
+    B2C_PK1X1("fused_1x1pkw_m128", 2, 2, 16, 4),
     // pointwise, 4-byte pixel staging (1x1, stride 1, no padding, any H*W)
     // (and strided 1x1, e.g. ResNet projection shortcuts)
     B2C_SCA1X1("fused_1x1s_m32", 1, 4, 16),
@@ -333,7 +348,7 @@ double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, in
   if (tc.kind == 5) lds_penalty = (g.S == 1 && (long long)g.H * g.W % 4 == 0) ? 1.15 : 0.9;
   if (tc.kind == 6) lds_penalty = 0.95;  // no per-thread staging, no CTA-wide barrier
   const double fma = (double)tc.bm * tc.bp * taps * tc.bc * tc.chunks_per_split * (stage1 ? 2.0 : 1.0) * lds_penalty;
-  const double per_elem = (tc.kind == 1 || (tc.kind == 5 && g.S == 1 && (long long)g.H * g.W % 4 == 0) || ((long long)g.H * g.W % 4 == 0 && (tc.kind == 0 || tc.kind >= 3))) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
+  const double per_elem = (tc.kind == 1 || tc.kind == 9 || (tc.kind == 5 && g.S == 1 && (long long)g.H * g.W % 4 == 0) || ((long long)g.H * g.W % 4 == 0 && (tc.kind == 0 || tc.kind >= 3))) ? 2.0 : 6.0;  // 16-byte groups vs 4-byte copies
   const double loads = (per_elem * tc.tile_elems + 4.0 * tc.bm * taps) * tc.bc * tc.chunks_per_split;
   const double fixed = 250000.0 + 12.0 * tc.tile_elems;
   const double split_io = tc.splits > 1 ? (double)tc.bm * tc.bp * 24.0 : 0.0;  // partial store per CTA
@@ -358,6 +373,9 @@ double model_cost(const Geom &g, const TileChoice &tc, int taps, bool stage1, in
   return t + reduce + 2.0e6;  // launch + ramp
 }
 
+// packed pointwise (kind 9): bytes of x'[C][qp] at the start of the workspace (partials follow)
+long long packed_bytes(const Geom &g) { return (4LL * g.C * ((g.Q + 3) & ~3LL) + 255) & ~255LL; }
+
 bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits, bool allow_split,
               Candidate *out) {
   const Family &f = kFamilies[fam_id];
@@ -371,7 +389,8 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
   base.bc = f.bc;
   base.threads = f.threads;
   base.kind = f.kind;
-  if (f.kind == 1 || f.kind == 2 || f.kind == 5 || f.kind == 6) {
+  if (f.kind == 9 && !allow_split) return false;  // needs a workspace for the packed pixels
+  if (f.kind == 1 || f.kind == 2 || f.kind == 5 || f.kind == 6 || f.kind == 9) {
     base.rs = g.W;
     base.rows = 1;
     base.tile_elems = f.bp;
@@ -408,7 +427,13 @@ bool evaluate(const Geom &g, int fam_id, bool stage1, int sms, int forced_splits
       const int by_smem = std::max(1, (int)((228LL * 1024) / (smem + 1024)));
       tc.occupancy = std::max(1, std::min({f.max_ctas_per_sm, by_smem, 2048 / f.threads}));
       tc.ws_bytes = tc.splits > 1 ? 4LL * tc.splits * g.N * g.M * g.HoWo : 0;
-      tc.cost = model_cost(g, tc, 1, false, sms, tc.occupancy) * (f.kind == 1 && f.tm == 2 ? 1.12 : 1.0);
+      tc.cost = model_cost(g, tc, 1, false, sms, tc.occupancy) * ((f.kind == 1 || f.kind == 9) && f.tm == 2 ? 1.12 : 1.0);
+      if (f.kind == 9) {  // + the packing pass: read the (strided) input rows, write x'[C][qp]
+        const long long qp = (g.Q + 3) & ~3LL;
+        tc.ws_bytes += packed_bytes(g);
+        const double moved = 4.0 * g.C * ((double)g.N * g.Ho * (g.S == 1 ? g.H / (double)g.Ho : 1.0) * g.W + qp);
+        tc.cost += 1.5e6 + 0.03 * moved;
+      }
       if (f.kind >= 5) tc.stages = f.stages;
       if (tc.cost < best.cost) {
         best.family = fam_id;
@@ -573,6 +598,9 @@ bool family_matches(int fam_id, const Geom &g, bool stage1) {
   if (f.kind == 2)
     return g.HF == 1 && g.WF == 1 && g.PH == 0 && g.PW == 0 && (g.S != 1 || ((long long)g.H * g.W) % 4 != 0) &&
            (long long)g.N * g.C * g.H * g.W < (1LL << 31);
+  if (f.kind == 9)  // where the 16-byte kernel cannot read x in place; fdiv-exact pixel indices
+    return !stage1 && g.HF == 1 && g.WF == 1 && g.PH == 0 && g.PW == 0 &&
+           (g.S != 1 || ((long long)g.H * g.W) % 4 != 0) && g.Q + 4 < kFdivLimit && g.C <= 65535;
   if (stage1) return g.S == 1;
   if (f.kind == 3 || f.kind == 4)
     return f.hf == g.HF && f.wf == g.WF && f.s == g.S && (long long)g.N * g.Ho * g.Wo < (1LL << 30);
@@ -836,7 +864,7 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   p.chunks_per_split = tc.splits > 1 ? tc.chunks_per_split : p.nchunks;
   if (tc.splits > 1) {
     if (!workspace) return cudaErrorInvalidValue;
-    p.partials = static_cast<float *>(workspace);
+    p.partials = reinterpret_cast<float *>(static_cast<char *>(workspace) + (f.kind == 9 ? packed_bytes(g) : 0));
     p.part_stride = (long long)g.N * g.M * g.HoWo;
   }
   p.w_ctaps = g.HF * g.WF;
@@ -848,6 +876,16 @@ cudaError_t launch_direct(const Geom &g, const TileChoice &tc, const float *x, c
   p.mHoWo = fdiv_magic(g.HoWo);
   p.mWo = fdiv_magic(g.Wo);
   p.pdl = pdl_enabled() ? 1 : 0;
+  if (f.kind == 9) {  // pack the (strided) pixels into x'[C][qp], then convolve x'
+    if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15)) return cudaErrorInvalidValue;
+    p.qp = (int)((g.Q + 3) & ~3LL);
+    float *xp = static_cast<float *>(workspace);
+    note_launch();
+    pack_pixels_kernel<<<dim3((unsigned)cdiv(p.qp / 4, 256), (unsigned)g.C), 256, 0, stream>>>(p, x, xp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    p.x = xp;
+  }
   dim3 grid((unsigned)tc.grid, (unsigned)tc.splits, (unsigned)tc.grid_z);
   // development tracing (-DB2C_DEV builds): per-CTA SM id and start/end globaltimer to a CSV file
 #ifdef B2C_DEV

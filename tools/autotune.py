@@ -100,6 +100,9 @@ def main():
                 if key in seen or (args.layers and cfg.name not in args.layers.split(",")):
                     continue
                 seen.add(key)
+                if args.families and "fused" in engines and not any(
+                        any(k in names[f] for k in args.families.split(",")) for f in matching_families(cfg)):
+                    continue  # no candidate family for this shape
                 if time.time() - t_start > args.budget_s:
                     break
                 x = torch.rand((cfg.n, cfg.c, cfg.h, cfg.w), device="cuda")

@@ -43,7 +43,7 @@ def main():
         fams = pk.matching_families(cfg)
         if quick:  # two round-1 families plus every row-segment / warp-specialised one
             names = pk.family_names()
-            fams = fams[:2] + [f for f in fams[2:] if any(k in names[f] for k in ("row7", "rws7", "1x1ws", "1x1t_"))]
+            fams = fams[:2] + [f for f in fams[2:] if any(k in names[f] for k in ("row7", "rws7", "1x1ws", "1x1t_", "1x1pk"))]
         for fam in fams:
             for splits, reduce in ((1, 0), (2, 1), (2, 2)):
                 try:
