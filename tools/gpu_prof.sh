@@ -28,7 +28,7 @@ timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --l
 fi
 if [ -z "$SKIP_TRAFFIC" ]; then
 timeout 900 $NCU --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-  -k regex:"conv|stage2" --csv --log-file "$OUT/traffic_ncu.csv" python tools/traffic.py run ${TRAFFIC_WL:-$WL} > "$OUT/traffic_layers.json" 2> "$OUT/traffic.err"
+  -k regex:"conv|stage2|pack" --csv --log-file "$OUT/traffic_ncu.csv" python tools/traffic.py run ${TRAFFIC_WL:-$WL} > "$OUT/traffic_layers.json" 2> "$OUT/traffic.err"
 fi
 for L in $LAYERS; do
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:conv -s 3 -c 1 \

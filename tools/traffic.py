@@ -1,7 +1,7 @@
 """Measured DRAM traffic per layer for bench.py's roofline (GPU box, under ncu).
 
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-        --clock-control none -k regex:"conv|stage2" --csv --log-file gpurun_out/tr/ncu.csv \
+        --clock-control none -k regex:"conv|stage2|pack" --csv --log-file gpurun_out/tr/ncu.csv \
         python tools/traffic.py run c1,c2,c3,c4,c5 > gpurun_out/tr/layers.json
     python tools/traffic.py merge gpurun_out/tr/layers.json gpurun_out/tr/ncu.csv > profiles/r1_traffic.json
 
@@ -9,7 +9,7 @@
 and with the plan bench.py uses (fused engine), and prints the ordered list of
 (workload, layer, plan, expected b2c launches).  `merge` walks ncu's launch
 list in the same order and sums the DRAM bytes of each layer's launches (conv
-kernel + split-C stage-2 sum): the "traffic" bench.py reports next to the
+kernel + split-C stage-2 sum + the packed path's pixel gather): the "traffic" bench.py reports next to the
 algorithmic bytes.  ncu replays each kernel with caches flushed, so these are
 cold-cache bytes per launch.
 """
@@ -41,7 +41,7 @@ def run(workloads):
             L = ConvLayer(c, "fused")
             L(x, w, out=y)
             torch.cuda.synchronize()
-            n = 2 if (L.splits > 1 and L.reduce != 2) else 1
+            n = (2 if (L.splits > 1 and L.reduce != 2) else 1) + (1 if "1x1pk" in L.family else 0)  # + pixel packing
             order.append({"workload": wl, "layer": c.name, "family": L.family, "launches": n,
                           "alg_bytes": c.compulsory_bytes, "flops": c.flops})
         del xs, ws, ys
