@@ -97,7 +97,10 @@ typedef struct {
   int32_t splits;       /* fused: channel ranges reduced separately (split-C);
                            on input to b2c_select_tiles / b2c_conv2d_forward,
                            > 0 forces the split                              */
-  int64_t workspace_bytes; /* workspace the plan needs (0 unless splits > 1) */
+  int64_t workspace_bytes; /* workspace the plan needs: split-C partial planes
+                              (splits > 1) and, for the packed-pixel pointwise
+                              families (fused_1x1pk*), the packed input
+                              4*C*ceil4(N*Ho*Wo) bytes; 0 otherwise          */
   int32_t reduce;       /* split-C reduction (splits > 1): 1 = partial planes in
                            the workspace + a stage-2 sum kernel, 2 = inside a
                            thread-block cluster through DSMEM (one kernel; same
@@ -203,8 +206,12 @@ b2c_status b2c_register_tuned_plan(const b2c_conv_desc *d, int32_t engine, int32
  * in `workspace` (tiles.workspace_bytes from b2c_select_tiles,
  * splits*N*M*Ho*Wo*4 bytes) and a second launch that adds them in ascending
  * range order, or (reduce = 2) inside a thread-block cluster through DSMEM in
- * the same order (one launch).  With no (or too small a) workspace the planner
- * picks an unsplit plan.  Per output, the summation order is a function of
+ * the same order (one launch).  Strided 1x1 layers and 1x1 layers on planes
+ * with H*W % 4 != 0 may run the packed-pixel path: a first launch gathers the
+ * pixels the layer reads into the head of `workspace`, the convolution reads
+ * them from there.  With no (or too small a) workspace the planner picks an
+ * unsplit, unpacked plan (a forced plan that needs one fails with
+ * B2C_INVALID_ARGUMENT).  Per output, the summation order is a function of
  * (c, hf, wf, splits) only: both reductions give bitwise-identical results. */
 b2c_status b2c_conv2d_forward(const b2c_conv_desc *d, const float *x, const float *w, float *y, void *workspace,
                               int64_t workspace_size, const b2c_tile_plan *tiles, void *stream);
