@@ -256,9 +256,13 @@ def test_tile_planner_covers_every_baseline_layer(native):
                 assert t.grid == tiles * t.splits, (wl, cfg.name)
                 chunks = -(-cfg.c // t.bc)
                 assert 1 <= t.splits <= chunks
-                assert (t.workspace_bytes > 0) == (t.splits > 1)
-                if t.splits > 1:
-                    assert t.workspace_bytes == 4 * t.splits * cfg.n * cfg.m * ho * wo
+                # packed-pixel pointwise plans keep the gathered input x'[C][ceil4(Q)] at the head of
+                # the workspace (256-byte aligned), the split-C partial planes after it
+                packed = ((4 * cfg.c * (-(-(cfg.n * ho * wo) // 4) * 4) + 255) // 256 * 256
+                          if "_1x1pk" in t.family else 0)
+                assert (t.workspace_bytes > 0) == (t.splits > 1 or packed > 0)
+                split_bytes = 4 * t.splits * cfg.n * cfg.m * ho * wo if t.splits > 1 else 0
+                assert t.workspace_bytes == packed + split_bytes, (wl, cfg.name, t.family)
                 if cfg.stride == 1:
                     s = pk.select_tiles(cfg, "twostage")
                     assert s.family.startswith("stage1_strict") and s.splits == 1

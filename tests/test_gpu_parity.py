@@ -343,3 +343,59 @@ def test_cluster_split_reduction_bitwise_equals_partial_planes(cfg):
             assert a.cpu().numpy().tobytes() == b.cpu().numpy().tobytes(), (dsm.family, splits)
             n += 1
     assert n > 0
+
+
+@pytest.mark.parametrize("cfg", [
+    pk.ConvConfig("pk7", n=5, c=40, h=7, w=7, m=72, hf=1, wf=1),                  # H*W % 4 != 0
+    pk.ConvConfig("pks2", n=3, c=24, h=14, w=14, m=40, hf=1, wf=1, stride=2),     # projection shortcut
+    pk.ConvConfig("pks2odd", n=2, c=20, h=15, w=13, m=33, hf=1, wf=1, stride=2),  # ragged Q, M tail
+], ids=lambda c: c.name)
+def test_packed_pointwise_through_c_abi(cfg):
+    """Packed-pixel pointwise families (kind 9) through b2c_conv2d_forward: the
+    plan's workspace holds the gathered pixels (+ partial planes when split);
+    a forced packed plan without it fails with B2C_INVALID_ARGUMENT; results
+    are bitwise those of the 4-byte-staged family with the same split ranges
+    and within tol(K) of the f64 oracle."""
+    import ctypes
+
+    import oracle
+    import torch
+
+    from paper_2103_16234_b200 import _native as nat
+
+    lib = nat.lib()
+    names = pk.family_names()
+    fams = [f for f in pk.matching_families(cfg) if "_1x1pk" in names[f]]
+    ref_fam = next(f for f in pk.matching_families(cfg) if names[f] == "fused_1x1s_m64")
+    assert fams
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.rand((cfg.n, cfg.c, cfg.h, cfg.w), generator=g, device="cuda") * 2 - 1
+    w = torch.rand((cfg.m, cfg.c, cfg.hf, cfg.wf), generator=g, device="cuda") * 2 - 1
+    ref = oracle.conv_f64(cfg, x.cpu().numpy(), w.cpu().numpy())
+    d = nat.desc(cfg)
+    stream = torch.cuda.current_stream().cuda_stream
+    for splits in (1, 2):
+        base = pk.ConvLayer(cfg, family=ref_fam, splits=splits, reduce=1)(x, w)
+        for f in fams:
+            plan = nat.TilePlanC()
+            plan.family, plan.splits, plan.reduce = f, splits, 1
+            if lib.b2c_select_tiles(ctypes.byref(d), nat.ENGINE_FUSED, ctypes.byref(plan)) != nat.OK:
+                assert splits > -(-cfg.c // 32)  # only a 32-channel chunk family can lack a second range
+                continue
+            assert plan.workspace_bytes >= 4 * cfg.c * cfg.n * ((cfg.h - 1) // cfg.stride + 1) * \
+                ((cfg.w - 1) // cfg.stride + 1)
+            y = torch.full(base.shape, float("nan"), device="cuda")
+            assert lib.b2c_conv2d_forward(ctypes.byref(d), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                          ctypes.c_void_p(y.data_ptr()), None, 0, ctypes.byref(plan),
+                                          ctypes.c_void_p(stream)) == nat.INVALID_ARGUMENT
+            ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device="cuda")
+            assert lib.b2c_conv2d_forward(ctypes.byref(d), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                          ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                          plan.workspace_bytes, ctypes.byref(plan), ctypes.c_void_p(stream)) == nat.OK
+            torch.cuda.synchronize()
+            assert oracle.relative_error(y.cpu().numpy(), ref) <= oracle.fp32_tolerance(cfg.c, 1, 1)
+            def first_bound(bc):  # end of the first split channel range
+                return min(cfg.c, -(-(-(-cfg.c // bc)) // splits) * bc)
+
+            if splits == 1 or first_bound(plan.bc) == first_bound(16):  # same ranges as the 16-channel reference
+                assert torch.equal(y, base), (names[f], splits)
