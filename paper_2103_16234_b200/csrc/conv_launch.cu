@@ -114,6 +114,16 @@ struct Family {
         RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::MIN_BLOCKS, 4, ST, 2, RX                                  \
   }
 
+// ... with NP producer warps
+#define B2C_ROWWSP2(NAME, HF, WF, S, RX, WM, WP, BC, ST)                                                  \
+  Family {                                                                                                 \
+    NAME, HF, WF, S, RowWsTile<HF, WF, S, RX, WM, WP, BC, ST, 2>::BM,                                      \
+        RowWsTile<HF, WF, S, RX, WM, WP, BC, ST, 2>::SEG * RX, BC, false,                                  \
+        RowWsTile<HF, WF, S, RX, WM, WP, BC, ST, 2>::NT,                                                   \
+        reinterpret_cast<const void *>(&conv_row_ws_kernel<HF, WF, S, RX, WM, WP, BC, ST, 2>),             \
+        RowWsTile<HF, WF, S, RX, WM, WP, BC, ST, 2>::MIN_BLOCKS, 4, ST, 2, RX                               \
+  }
+
 // warp-specialised pointwise kernel (kind 5)
 #define B2C_PW1X1WS(NAME, WM, WP, BC, ST)                                                                   \
   Family {                                                                                                 \
@@ -203,12 +213,17 @@ const Family kFamilies[] = {
     B2C_ROW("fused_5x5s1_row7_m32", 5, 5, 1, 7, 2, 2, 4, 3),
     B2C_ROW("fused_7x7s2_row7_m64", 7, 7, 2, 7, 4, 1, 4, 2),
     B2C_ROWWS("fused_3x3s1_rws7_m64", 3, 3, 1, 7, 4, 1, 8, 3),
+    B2C_ROWWSP2("fused_3x3s1_rws7_m64p2", 3, 3, 1, 7, 4, 1, 8, 3),
     B2C_ROWWS("fused_3x3s1_rws7_m64w2", 3, 3, 1, 7, 4, 2, 8, 4),
     B2C_ROWWS("fused_3x3s1_rws7_m32", 3, 3, 1, 7, 2, 2, 8, 3),
     B2C_ROWWS("fused_3x3s1_rws7_m128", 3, 3, 1, 7, 8, 1, 8, 3),
     B2C_ROWWS("fused_3x3s2_rws7_m64", 3, 3, 2, 7, 4, 1, 8, 3),
     B2C_ROWWS("fused_3x3s2_rws7_m128", 3, 3, 2, 7, 8, 1, 8, 3),
+    B2C_ROWWSP2("fused_3x3s2_rws7_m128p2", 3, 3, 2, 7, 8, 1, 8, 3),
+    B2C_ROWWSP2("fused_3x3s2_rws7_m64p2", 3, 3, 2, 7, 4, 1, 8, 3),
+    B2C_ROWWSP2("fused_3x3s2_rws7_m64c4p2", 3, 3, 2, 7, 4, 1, 4, 3),
     B2C_ROWWS("fused_5x5s1_rws7_m64", 5, 5, 1, 7, 4, 1, 4, 3),
+    B2C_ROWWSP2("fused_5x5s1_rws7_m64p2", 5, 5, 1, 7, 4, 1, 4, 3),
     B2C_ROWWS("fused_5x5s1_rws7_m32", 5, 5, 1, 7, 2, 2, 4, 3),
     B2C_ROWWS("fused_7x7s2_rws7_m64", 7, 7, 2, 7, 4, 1, 4, 2),
     // stride 2 on small planes: the band is ~2x the output rows, so 4-channel stages keep 2 CTAs per SM
@@ -219,6 +234,7 @@ const Family kFamilies[] = {
     B2C_ROWWS("fused_7x7s2_rws7_m32st1", 7, 7, 2, 7, 2, 2, 4, 1),
     // 3-channel stages (ResNet conv1): the filter rows of a tile are one contiguous bulk copy
     B2C_ROWWS("fused_7x7s2_rws7_m64c3", 7, 7, 2, 7, 4, 1, 3, 1),
+    B2C_ROWWSP2("fused_7x7s2_rws7_m64c3p2", 7, 7, 2, 7, 4, 1, 3, 1),
     B2C_ROWWS("fused_7x7s2_rws7_m32c3", 7, 7, 2, 7, 2, 2, 3, 1),
     // persistent warp-specialised pointwise families (conv1x1_ws.cuh)
     B2C_PW1X1WS("fused_1x1ws_m64", 4, 2, 16, 4),

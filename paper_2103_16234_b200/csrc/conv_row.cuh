@@ -211,13 +211,16 @@ __global__ void __launch_bounds__(RowTile<HF, WF, S, RX, WM, WP, BC, MINB>::NT, 
 // every channel and stage), so the producer never stores to shared memory.
 // Consumers read the 16 filters of a (channel, tap) as 16 broadcast scalar
 // loads (one wavefront each — the same crossbar cost as 4 LDS.128).
-template <int HF, int WF, int S, int RX, int WM, int WP, int BC, int ST>
+// NP = producer warps: 2 for stride-2 bands staged by 4-byte copies (4x the
+// cp.async instructions of a 16-byte-staged band), where one producer warp
+// sharing its sub-partition with FFMA2-bound consumers starves them
+template <int HF, int WF, int S, int RX, int WM, int WP, int BC, int ST, int NP = 1>
 struct RowWsTile {
   static constexpr int RM = 16;
   static constexpr int BM = RM * WM;
   static constexpr int SEG = 32 * WP;
   static constexpr int NCW = WM * WP;             // consumer warps
-  static constexpr int NT = 32 * (NCW + 1);       // + one producer warp
+  static constexpr int NT = 32 * (NCW + NP);      // + the producer warps
   static constexpr int TAPS = HF * WF;
   static constexpr int WROW = BC * TAPS;          // filter tile row (floats)
   static constexpr int WFLOATS = BM * WROW;       // multiple of 32: stages stay 128-byte aligned
@@ -227,11 +230,11 @@ struct RowWsTile {
   static_assert(ST >= 1 && ST <= 14, "one named barrier per stage (ids 1..ST; 15: cluster epilogue)");
 };
 
-template <int HF, int WF, int S, int RX, int WM, int WP, int BC, int ST>
-__global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
-                                  RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::MIN_BLOCKS)
+template <int HF, int WF, int S, int RX, int WM, int WP, int BC, int ST, int NP = 1>
+__global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST, NP>::NT,
+                                  RowWsTile<HF, WF, S, RX, WM, WP, BC, ST, NP>::MIN_BLOCKS)
     conv_row_ws_kernel(const __grid_constant__ KParams p, const __grid_constant__ CUtensorMap wmap) {
-  using T = RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>;
+  using T = RowWsTile<HF, WF, S, RX, WM, WP, BC, ST, NP>;
   constexpr int RM = T::RM, BM = T::BM, SEG = T::SEG, NCW = T::NCW, TAPS = T::TAPS, WROW = T::WROW;
   constexpr int WFLOATS = T::WFLOATS, PXN = T::PXN;
 
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
 
   if (tid == 0) {
     for (int s = 0; s < ST; s++) {
-      mbar_init(smem_u32(&bars[s]), 32);        // producer lanes' arrivals (+ TMA bytes)
+      mbar_init(smem_u32(&bars[s]), 32 * NP);   // producer threads' arrivals (+ TMA bytes)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -279,8 +282,9 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
   const int chunk_end = min(p.nchunks, chunk_begin + p.chunks_per_split);
   if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (wid == NCW) {
-    // ---------------- producer warp ----------------
+  if (wid >= NCW) {
+    // ---------------- producer warp(s) ----------------
+    const int pt0 = (wid - NCW) * 32 + lane;  // producer thread index
     const float *xtile = p.x + (long long)n0 * chw;
     const bool tma = p.w_tma != 0;
     for (int chunk = chunk_begin; chunk < chunk_end; chunk++) {
@@ -295,13 +299,13 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
       if (p.w_tma == 2) {
         // the family's chunk is all C channels (BC == C): the tile's filter rows
         // are one contiguous block of the caller's tensor -> one bulk copy
-        if (lane == 0) {
+        if (pt0 == 0) {
           const uint32_t bytes = 4u * (uint32_t)min(BM, p.M - m0) * WROW;
           mbar_expect_tx_only(full, bytes);
           bulk_copy_g2s(smem_u32(wst), p.w + (long long)m0 * WROW, bytes, full);
         }
       } else if (tma) {
-        if (lane == 0) {
+        if (pt0 == 0) {
           mbar_expect_tx_only(full, WFLOATS * 4);
           tma_load_2d(smem_u32(wst), &wmap, c0 * TAPS, m0, full);
         }
@@ -309,9 +313,10 @@ __global__ void __launch_bounds__(RowWsTile<HF, WF, S, RX, WM, WP, BC, ST>::NT,
         const int ctv = cvalid * TAPS;
         const float *wsrc = p.w + (long long)m0 * p.C * TAPS + (long long)c0 * TAPS;
         for (int m = 0; m < BM && m0 + m < p.M; m++)
-          for (int ct = lane; ct < ctv; ct += 32) cp_async4(wst + m * WROW + ct, wsrc + (long long)m * p.C * TAPS + ct);
+          for (int ct = pt0; ct < ctv; ct += 32 * NP)
+            cp_async4(wst + m * WROW + ct, wsrc + (long long)m * p.C * TAPS + ct);
       }
-      stage_halo_chunk<BC, false>(p, goff, gtab, wst + WFLOATS, xtile + (long long)c0 * hw, cvalid, hw, lane, 32);
+      stage_halo_chunk<BC, false>(p, goff, gtab, wst + WFLOATS, xtile + (long long)c0 * hw, cvalid, hw, pt0, 32 * NP);
       cp_async_mbar_arrive_noinc(full);  // the arrive fires when this thread's copies have landed
     }
     if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
