@@ -214,6 +214,7 @@ const Family kFamilies[] = {
     B2C_ROW("fused_7x7s2_row7_m64", 7, 7, 2, 7, 4, 1, 4, 2),
     B2C_ROWWS("fused_3x3s1_rws7_m64", 3, 3, 1, 7, 4, 1, 8, 3),
     B2C_ROWWSP2("fused_3x3s1_rws7_m64p2", 3, 3, 1, 7, 4, 1, 8, 3),
+    B2C_ROWWSP2("fused_3x3s1_rws7_m64c12st2p2", 3, 3, 1, 7, 4, 1, 12, 2),
     B2C_ROWWS("fused_3x3s1_rws7_m64w2", 3, 3, 1, 7, 4, 2, 8, 4),
     B2C_ROWWS("fused_3x3s1_rws7_m32", 3, 3, 1, 7, 2, 2, 8, 3),
     B2C_ROWWS("fused_3x3s1_rws7_m128", 3, 3, 1, 7, 8, 1, 8, 3),
